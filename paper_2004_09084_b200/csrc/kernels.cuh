@@ -1,0 +1,488 @@
+// kernels.cuh -- device kernels of the layered decoder (sm_100a).
+//
+// Device layouts.  Codewords are interleaved in groups of W
+// lanes (W a power of two <= 32, Bp = G*W >= B, b = g*W + w):
+//   llr, posterior L : T[G][n][W]           element (v, b) at (g*n + v)*W + w
+//   edge messages R  : T[G][E][z][W]        edge e (slot order), offset k
+//   syndrome         : u8[G][S][z][W]       slot order (the reference indexes the
+//                                           ORIGINAL row, decoder.py:168-170; the
+//                                           upload kernel applies the permutation)
+// A thread owns one check (slot s, offset k) for V consecutive lanes w0..w0+V-1.
+// Consecutive threads walk (k, w), so for every edge j of the check a warp reads and
+// writes one contiguous run of L (variables col*z + (k+shift) mod z are consecutive
+// in k) and one contiguous run of R: every access is a coalesced V*sizeof(T)-wide
+// vector access and each algorithmic byte crosses the memory system once.
+#pragma once
+#include <cstdint>
+
+#include "phi.cuh"
+#include "philox.cuh"
+
+namespace qcl {
+
+constexpr int kBlock = 256;
+
+struct SlotInfo {      // one rearranged row slot of H_compact1
+    int32_t edge_off;  // first circulant (slot order)
+    int32_t degree;
+    int32_t row;       // original base row
+    int32_t pad;
+};
+struct EdgeInfo {      // one circulant of H_compact1
+    int32_t var_base;  // base_col * z
+    int32_t shift;
+};
+
+// Everything a launch over a contiguous slot range needs.
+struct SlotRange {
+    const SlotInfo *slots;
+    const EdgeInfo *edges;
+    int64_t n;        // variables per codeword
+    int32_t E;        // circulants
+    int32_t S;        // slots (all layers)
+    int32_t z;
+    int32_t slot0;    // first slot of the launch
+    int32_t nslots;   // slots in the launch
+    int32_t bps;      // blocks per (group, slot)
+    int32_t lw;       // log2 W
+};
+
+struct LayerArgs {
+    SlotRange r;
+    void *L;
+    void *R;
+    const uint8_t *syn;  // nullptr: all-zero target
+    int32_t uniform;     // uniform row degree in the layer (FP64 fold order)
+    double clip, eps;
+};
+
+template <typename T, int V> struct Vec;
+template <> struct Vec<float, 1> { using type = float; };
+template <> struct Vec<float, 2> { using type = float2; };
+template <> struct Vec<float, 4> { using type = float4; };
+template <> struct Vec<double, 1> { using type = double; };
+template <> struct Vec<double, 2> { using type = double2; };
+
+// L2-only (.cg) accesses: state is produced by other CTAs between launches/barriers,
+// and nothing is re-read within a layer, so L1 allocation would only risk staleness.
+template <typename T, int V>
+__device__ __forceinline__ void vload(const T *p, T (&out)[V]) {
+    using VT = typename Vec<T, V>::type;
+    VT v = __ldcg(reinterpret_cast<const VT *>(p));
+    const T *s = reinterpret_cast<const T *>(&v);
+#pragma unroll
+    for (int i = 0; i < V; i++) out[i] = s[i];
+}
+template <typename T, int V>
+__device__ __forceinline__ void vstore(T *p, const T (&in)[V]) {
+    using VT = typename Vec<T, V>::type;
+    VT v;
+    T *d = reinterpret_cast<T *>(&v);
+#pragma unroll
+    for (int i = 0; i < V; i++) d[i] = in[i];
+    __stcg(reinterpret_cast<VT *>(p), v);
+}
+
+__device__ __forceinline__ float clampT(float x, float c) { return fminf(fmaxf(x, -c), c); }
+__device__ __forceinline__ double clampT(double x, double c) { return fmin(fmax(x, -c), c); }
+
+template <typename T> __device__ __forceinline__ T phiT(T x, T eps, T clip);
+template <> __device__ __forceinline__ float phiT<float>(float x, float eps, float clip) {
+    return phi_fast(x, eps, clip);
+}
+template <> __device__ __forceinline__ double phiT<double>(double x, double eps, double clip) {
+    return phi_ref(x, eps, clip);
+}
+
+// numpy pairwise_sum of a[1..d) (d-1 <= 31 terms), restated for the FP64 parity path:
+// fewer than 8 terms is a left fold started from 0.0; otherwise 8 strided accumulators
+// combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail (decoder.py:240,
+// np.add.reduceat = a0 + pairwise(rest), measured in SURVEY.md Appendix B P3).
+template <int DMAX>
+__device__ __forceinline__ double pairwise_rest(const double (&a)[DMAX], int d) {
+    const int cnt = d - 1;
+    if (cnt < 8) {
+        double r = 0.0;
+#pragma unroll
+        for (int j = 1; j < DMAX; j++)
+            if (j < d) r += a[j];
+        return r;
+    }
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) acc[i] = a[1 + i < DMAX ? 1 + i : 0];
+    const int body = cnt - (cnt % 8);
+#pragma unroll
+    for (int j = 9; j < DMAX; j++)
+        if (j - 1 < body) acc[(j - 1) & 7] += a[j];
+    double res = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+    for (int j = 1; j < DMAX; j++)
+        if (j - 1 >= body && j < d) res += a[j];
+    return res;
+}
+
+// Map blockIdx.x -> (group, slot, k, w0) for a launch over a slot range.
+struct Item {
+    int g, slot, k, w0;
+    bool live;
+};
+template <int V>
+__device__ __forceinline__ Item map_item(const SlotRange &r) {
+    int blk = blockIdx.x;
+    const int chunk = blk % r.bps;
+    blk /= r.bps;
+    Item it;
+    it.slot = r.slot0 + blk % r.nslots;
+    it.g = blk / r.nslots;
+    const int lanes_v = (1 << r.lw) / V;
+    const int item = chunk * kBlock + threadIdx.x;
+    it.live = item < r.z * lanes_v;
+    it.k = item / lanes_v;
+    it.w0 = (item - it.k * lanes_v) * V;
+    return it;
+}
+
+// One layered update of every check in the launch's slot range, for every group.
+// Reference: decoder.py:212-250 (_layer_update_core), per check m and edge j:
+//   q_j = clip(L_v - r_old_j); ph_j = Phi(|q_j|); parity = XOR_j(q_j < 0) ^ s_m
+//   FP32 path: others_j = exclusive prefix + suffix sum of ph (avoids the FP32
+//              cancellation of total - own);
+//   FP64 path: others_j = total - ph_j with the reference's fold order;
+//   r_j = clip(+-Phi(others_j)) with sign (q_j<0)^parity; L_v = clip(q_j + r_j).
+// Rows of one merged layer touch disjoint columns (checked at plan creation,
+// decoder.py:144-154), so the read-modify-write of L is race free.
+template <typename T, int V, int DMAX, bool HAS_SYN>
+__global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
+    __shared__ EdgeInfo s_edge[DMAX];
+    const Item it = map_item<V>(a.r);
+    const SlotInfo si = a.r.slots[it.slot];
+    const int d = si.degree;
+    if (threadIdx.x < d) s_edge[threadIdx.x] = a.r.edges[si.edge_off + threadIdx.x];
+    __syncthreads();
+    if (!it.live) return;
+
+    const int z = a.r.z, lw = a.r.lw, k = it.k;
+    T *L = reinterpret_cast<T *>(a.L);
+    T *R = reinterpret_cast<T *>(a.R);
+    const T clip = (T)a.clip, eps = (T)a.eps;
+    const int64_t lbase = (int64_t)it.g * a.r.n;
+    const int64_t rbase = ((int64_t)it.g * a.r.E + si.edge_off) * z + k;
+
+    T q[DMAX][V], ph[DMAX][V];
+    int64_t laddr[DMAX];
+    int par[V];
+    if (HAS_SYN) {
+        const uint8_t *sp = a.syn + ((((int64_t)it.g * a.r.S + it.slot) * z + k) << lw) + it.w0;
+#pragma unroll
+        for (int i = 0; i < V; i++) par[i] = sp[i] & 1;
+    } else {
+#pragma unroll
+        for (int i = 0; i < V; i++) par[i] = 0;
+    }
+    // gather: all 2d loads issued before any use (memory-level parallelism)
+#pragma unroll
+    for (int j = 0; j < DMAX; j++) {
+        if (j < d) {
+            int pos = k + s_edge[j].shift;
+            pos -= (pos >= z) ? z : 0;
+            laddr[j] = ((lbase + s_edge[j].var_base + pos) << lw) + it.w0;
+            T lv[V], rv[V];
+            vload<T, V>(L + laddr[j], lv);
+            vload<T, V>(R + ((rbase + (int64_t)j * z) << lw) + it.w0, rv);
+#pragma unroll
+            for (int i = 0; i < V; i++) q[j][i] = clampT(lv[i] - rv[i], clip);
+        } else {
+#pragma unroll
+            for (int i = 0; i < V; i++) q[j][i] = (T)0;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < DMAX; j++) {
+#pragma unroll
+        for (int i = 0; i < V; i++) {
+            if (j < d) {
+                ph[j][i] = phiT<T>(q[j][i] < (T)0 ? -q[j][i] : q[j][i], eps, clip);
+                par[i] ^= (q[j][i] < (T)0);
+            } else {
+                ph[j][i] = (T)0;
+            }
+        }
+    }
+    // others_j, in place in ph
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int i = 0; i < V; i++) {
+            T pre = 0, suf = 0, tmp[DMAX];
+#pragma unroll
+            for (int j = 0; j < DMAX; j++) {
+                tmp[j] = pre;
+                pre += ph[j][i];
+            }
+#pragma unroll
+            for (int j = DMAX - 1; j >= 0; j--) {
+                T p = ph[j][i];
+                ph[j][i] = tmp[j] + suf;
+                suf += p;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < V; i++) {
+            double col[DMAX];
+#pragma unroll
+            for (int j = 0; j < DMAX; j++) col[j] = ph[j][i];
+            double total;
+            if (a.uniform) {
+                total = col[0];
+#pragma unroll
+                for (int j = 1; j < DMAX; j++)
+                    if (j < d) total += col[j];
+            } else {
+                total = col[0] + pairwise_rest<DMAX>(col, d);
+            }
+#pragma unroll
+            for (int j = 0; j < DMAX; j++) ph[j][i] = total - col[j];
+        }
+    }
+    // scatter
+#pragma unroll
+    for (int j = 0; j < DMAX; j++) {
+        if (j < d) {
+            T rv[V], lv[V];
+#pragma unroll
+            for (int i = 0; i < V; i++) {
+                T mag = phiT<T>(ph[j][i], eps, clip);
+                bool neg = (q[j][i] < (T)0) ^ (par[i] != 0);
+                rv[i] = clampT(neg ? -mag : mag, clip);
+                lv[i] = clampT(q[j][i] + rv[i], clip);
+            }
+            vstore<T, V>(R + ((rbase + (int64_t)j * z) << lw) + it.w0, rv);
+            vstore<T, V>(L + laddr[j], lv);
+        }
+    }
+}
+
+// Parity of the hard decision of every check vs the target syndrome; any unsatisfied
+// check of codeword b sets unsat[b] (syndrome_satisfied, decoder.py:268-273).
+template <typename T>
+__global__ void __launch_bounds__(kBlock) check_kernel(SlotRange r, const T *L, const uint8_t *syn,
+                                                       uint8_t *unsat) {
+    __shared__ EdgeInfo s_edge[64];
+    const Item it = map_item<1>(r);
+    const SlotInfo si = r.slots[it.slot];
+    for (int j = threadIdx.x; j < si.degree && j < 64; j += kBlock) s_edge[j] = r.edges[si.edge_off + j];
+    __syncthreads();
+    if (!it.live) return;
+    const int64_t lbase = (int64_t)it.g * r.n;
+    int p = syn ? (syn[((((int64_t)it.g * r.S + it.slot) * r.z + it.k) << r.lw) + it.w0] & 1) : 0;
+    for (int j = 0; j < si.degree; j++) {
+        EdgeInfo e = j < 64 ? s_edge[j] : r.edges[si.edge_off + j];
+        int pos = it.k + e.shift;
+        pos -= (pos >= r.z) ? r.z : 0;
+        T v = __ldcg(L + ((lbase + e.var_base + pos) << r.lw) + it.w0);
+        p ^= (v < (T)0);
+    }
+    if (p) unsat[(it.g << r.lw) + it.w0] = 1;
+}
+
+// Hard decisions (decoder.py:264-266: bit = L < 0, so -0.0 -> 0) of the codewords with
+// take[b] != 0, transposed from T[G][n][W] into the reference's (B, n) byte layout
+// through a 64-variable x 32-codeword shared tile.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) words_kernel(const T *L, int64_t n, int lw, int64_t B,
+                                                       const uint8_t *take, uint8_t *words) {
+    __shared__ uint8_t tile[32][64 + 4];
+    const int64_t v0 = (int64_t)blockIdx.x * 64;
+    const int64_t b0 = (int64_t)blockIdx.y * 32;
+    const int Wm = (1 << lw) - 1;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        int e = i * kBlock + threadIdx.x;
+        int bl = e & 31, vl = e >> 5;
+        int64_t b = b0 + bl, v = v0 + vl;
+        uint8_t bit = 0;
+        if (b < B && v < n) {
+            int64_t g = b >> lw, w = b & Wm;
+            bit = __ldcg(L + ((g * n + v) << lw) + w) < (T)0;
+        }
+        tile[bl][vl] = bit;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+        int e = i * kBlock + threadIdx.x;
+        int vl = e & 63, bl = e >> 6;
+        int64_t b = b0 + bl, v = v0 + vl;
+        if (b < B && v < n && (take == nullptr || take[b])) words[b * n + v] = tile[bl][vl];
+    }
+}
+
+// Early-termination bookkeeping after sweep t (decoder.py:295-305): codewords whose
+// hard decision satisfies the syndrome for the first time freeze words/iterations.
+__global__ void et_update_kernel(int64_t B, int t, const uint8_t *unsat, uint8_t *active, uint8_t *take,
+                                 uint8_t *converged, int64_t *iterations, int *n_active) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    uint8_t newly = active[b] && !unsat[b];
+    take[b] = newly;
+    if (newly) {
+        active[b] = 0;
+        converged[b] = 1;
+        iterations[b] = t;
+        atomicSub(n_active, 1);
+    }
+}
+
+// End of decode for codewords still active (decoder.py:307-311).
+__global__ void finalize_kernel(int64_t B, const uint8_t *unsat, const uint8_t *active, uint8_t *take,
+                                uint8_t *converged) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    take[b] = active[b];
+    if (active[b]) converged[b] = !unsat[b];
+}
+
+__global__ void decode_init_kernel(int64_t B, int64_t Bp, int max_iter, uint8_t *active, uint8_t *converged,
+                                   int64_t *iterations, int *n_active) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b == 0) *n_active = (int)B;
+    if (b >= Bp) return;
+    active[b] = b < B;
+    if (b < B) {
+        converged[b] = 0;
+        iterations[b] = max_iter;
+    }
+}
+
+// Host (B, n) LLRs (f64 or f32) -> T[G][n][W], rows b >= B zero-filled.
+template <typename T, typename S>
+__global__ void llr_to_lanes_kernel(const S *src, int64_t B, int64_t Bp, int64_t n, int lw, T *dst) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over Bp * n, lane fastest
+    if (i >= Bp * n) return;
+    const int W = 1 << lw;
+    int64_t w = i & (W - 1);
+    int64_t rest = i >> lw;
+    int64_t v = rest % n, g = rest / n;
+    int64_t b = (g << lw) + w;
+    dst[i] = b < B ? (T)src[b * n + v] : (T)0;
+}
+
+// posterior = clip(llr), messages = 0 (new_state, decoder.py:191-202).  For the FP32
+// path the clip is applied in FP64 before the cast (inputs may be +-inf).
+template <typename T>
+__global__ void reset_kernel(const T *llr, T *L, int64_t count, double clip) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) L[i] = (T)clampT((double)llr[i], clip);
+}
+
+// Reference-layout FP64 state <-> lanes.  post (B, n); msg (B, E*z) [e][k].
+template <typename T>
+__global__ void state_in_kernel(const double *post, const double *msg, int64_t B, int64_t n, int64_t Ez,
+                                int lw, T *L, T *R, int64_t Bp) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int W = 1 << lw;
+    int64_t w = i & (W - 1), rest = i >> lw;
+    if (i < Bp * n) {
+        int64_t v = rest % n, g = rest / n, b = (g << lw) + w;
+        L[i] = b < B ? (T)post[b * n + v] : (T)0;
+    }
+    if (i < Bp * Ez) {
+        int64_t x = rest % Ez, g = rest / Ez, b = (g << lw) + w;
+        R[i] = (b < B && msg) ? (T)msg[b * Ez + x] : (T)0;
+    }
+}
+template <typename T>
+__global__ void state_out_kernel(const T *L, const T *R, int64_t B, int64_t n, int64_t Ez, int lw,
+                                 double *post, double *msg) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over B * max(n, Ez), row-major
+    int64_t b = i / (n > Ez ? n : Ez), x = i % (n > Ez ? n : Ez);
+    if (b >= B) return;
+    const int W = 1 << lw;
+    int64_t g = b >> lw, w = b & (W - 1);
+    if (post && x < n) post[b * n + x] = (double)L[((g * n + x) << lw) + w];
+    if (msg && x < Ez) msg[b * Ez + x] = (double)R[((g * Ez + x) << lw) + w];
+}
+
+// Target syndrome (B, m) in original row order -> u8[G][S][z][W] in slot order.
+__global__ void syndrome_to_lanes_kernel(const uint8_t *src, const SlotInfo *slots, int64_t B, int64_t Bp,
+                                         int S, int z, int lw, uint8_t *dst, int *any_set) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over Bp * S * z
+    if (i >= Bp * (int64_t)S * z) return;
+    const int W = 1 << lw;
+    int64_t w = i & (W - 1), rest = i >> lw;
+    int64_t k = rest % z;
+    rest /= z;
+    int64_t s = rest % S, g = rest / S, b = (g << lw) + w;
+    const int64_t m = (int64_t)S * z;
+    const uint8_t bit = b < B ? (src[b * m + (int64_t)slots[s].row * z + k] != 0) : 0;
+    dst[i] = bit;
+    if (bit) *any_set = 1;  // benign race: every writer stores 1
+}
+
+// Syndrome (lanes layout) of words (B, n) -- encode mode target H*c (bench.py:225-226).
+__global__ void __launch_bounds__(kBlock) syndrome_of_words_kernel(SlotRange r, const uint8_t *words,
+                                                                   int64_t B, uint8_t *syn) {
+    const Item it = map_item<1>(r);
+    if (!it.live) return;
+    const SlotInfo si = r.slots[it.slot];
+    const int64_t b = ((int64_t)it.g << r.lw) + it.w0;
+    int p = 0;
+    if (b < B) {
+        for (int j = 0; j < si.degree; j++) {
+            EdgeInfo e = r.edges[si.edge_off + j];
+            int pos = it.k + e.shift;
+            pos -= (pos >= r.z) ? r.z : 0;
+            p ^= words[b * r.n + e.var_base + pos] & 1;
+        }
+    }
+    syn[((((int64_t)it.g * r.S + it.slot) * r.z + it.k) << r.lw) + it.w0] = (uint8_t)p;
+}
+
+// Device BIAWGN channel (channel.py:41-56 semantics): frame b of the state is frame
+// first_frame + b; LLR = 2 (1 - 2c + sigma n) / sigma^2 written straight into the lanes
+// layout.  One thread = 4 consecutive variables of one frame (one Philox block).
+template <typename T>
+__global__ void synth_llr_kernel(int64_t B, int64_t Bp, int64_t n, int lw, uint64_t seed, uint32_t snr_idx,
+                                 int64_t first_frame, double sigma, double sigma2, int encode,
+                                 T *llr, uint8_t *truths) {
+    const int64_t quads = (n + 3) / 4;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // lane fastest
+    if (i >= Bp * quads) return;
+    const int W = 1 << lw;
+    int64_t w = i & (W - 1), rest = i >> lw;
+    int64_t qv = rest % quads, g = rest / quads, b = (g << lw) + w;
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    const uint64_t frame = (uint64_t)(first_frame + b);
+    u32x4 ctr{(uint32_t)qv, (uint32_t)frame, (uint32_t)(frame >> 32), snr_idx & 0x7fffffffu};
+    double nz[4];
+    normals4(philox4x32_10(ctr, k0, k1), nz);
+    uint32_t cbits = 0;
+    if (encode) {
+        u32x4 c2 = ctr;
+        c2.w |= 0x80000000u;
+        u32x4 rb = philox4x32_10(c2, k0, k1);
+        cbits = (rb.x & 1) | ((rb.y & 1) << 1) | ((rb.z & 1) << 2) | ((rb.w & 1) << 3);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        int64_t v = qv * 4 + j;
+        if (v >= n) break;
+        int c = (cbits >> j) & 1;
+        double r = (1.0 - 2.0 * c) + sigma * nz[j];
+        double val = b < B ? 2.0 * r / sigma2 : 0.0;
+        llr[((g * n + v) << lw) + w] = (T)val;
+        if (truths && b < B) truths[b * n + v] = (uint8_t)c;
+    }
+}
+
+__global__ void phi_array_kernel(const double *x, int64_t cnt, double eps, double clip, int prec, double *out) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= cnt) return;
+    if (prec == 0)
+        out[i] = (double)phi_fast((float)x[i], (float)eps, (float)clip);
+    else
+        out[i] = phi_ref(x[i], eps, clip);
+}
+
+}  // namespace qcl

@@ -31,6 +31,8 @@ struct SlotInfo {      // one rearranged row slot of H_compact1
 struct EdgeInfo {      // one circulant of H_compact1
     int32_t var_base;  // base_col * z
     int32_t shift;
+    int32_t reused;    // column degree > 1: its posteriors are re-read by later layers
+    int32_t pad;
 };
 
 // Everything a launch over a contiguous slot range needs.
@@ -41,7 +43,8 @@ struct SlotRange {
     int32_t E;        // circulants
     int32_t S;        // slots (all layers)
     int32_t z;
-    int32_t slot0;    // first slot of the launch
+    const int32_t *slot_list;  // launch unit's slots (nullptr: contiguous from slot0)
+    int32_t slot0;    // first slot (or first slot_list entry) of the launch
     int32_t nslots;   // slots in the launch
     int32_t bps;      // blocks per (group, slot)
     int32_t lw;       // log2 W
@@ -133,7 +136,8 @@ __device__ __forceinline__ Item map_item(const SlotRange &r) {
     const int chunk = blk % r.bps;
     blk /= r.bps;
     Item it;
-    it.slot = r.slot0 + blk % r.nslots;
+    const int si = r.slot0 + blk % r.nslots;
+    it.slot = r.slot_list ? r.slot_list[si] : si;
     it.g = blk / r.nslots;
     const int lanes_v = (1 << r.lw) / V;
     const int item = chunk * kBlock + threadIdx.x;

@@ -20,6 +20,7 @@
 
 #include "../../include/qcldpc_b200.h"
 #include "kernels.cuh"
+#include "pipeline.cuh"
 
 using namespace qcl;
 
@@ -52,6 +53,15 @@ struct qcl_plan {
     int max_degree = 0;
     std::vector<int32_t> layer_start;  // [n_layers + 1] slot ranges
     std::vector<int> layer_dmax, layer_uniform;
+    // launch units: the rows of a merged layer are independent, so a ragged layer is
+    // split by degree class and each class gets the kernel variant sized for it
+    struct Unit {
+        int layer, list_off, count, dmax;
+    };
+    std::vector<Unit> units;
+    std::vector<int> layer_unit0;  // [n_layers + 1]
+    int32_t *slot_list = nullptr;  // device: concatenated unit slot ids
+    std::vector<int32_t> h_slot_list;
     std::vector<SlotInfo> h_slots;
     SlotInfo *slots = nullptr;  // device H_compact1: per slot
     EdgeInfo *edges = nullptr;  // device H_compact1: per circulant
@@ -59,8 +69,12 @@ struct qcl_plan {
     std::vector<qcl_state *> cache;  // idle states reused by qcl_decode
 };
 
+constexpr int kSideStreams = 4;
+
 struct qcl_state {
     qcl_plan *plan = nullptr;
+    cudaStream_t side[kSideStreams] = {};
+    cudaEvent_t fork = nullptr, join[kSideStreams] = {};
     int64_t B = 0, Bp = 0;
     int prec = QCL_PREC_FP32, lw = 0, W = 1, G = 1;
     size_t esz = 4;
@@ -80,7 +94,7 @@ struct qcl_state {
     cudaGraphExec_t sweep_exec = nullptr;
     double g_clip = -1, g_eps = -1;
     bool g_syn = false;
-    int64_t launches_layer = 0, launches_all = 0;
+    int64_t launches_layer = 0, launches_all = 0, sweep_launches = 0;
     bool profiling = false;
     float layer_ms = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sweep_events;
@@ -125,9 +139,10 @@ static int vec_width(const qcl_state *st, int dmax) {
     return std::min(st->W, v);
 }
 
-static SlotRange slot_range(const qcl_state *st, int slot0, int nslots, int V) {
+static SlotRange slot_range(const qcl_state *st, int slot0, int nslots, int V, const int32_t *list = nullptr) {
     const qcl_plan *p = st->plan;
     SlotRange r;
+    r.slot_list = list;
     r.slots = p->slots;
     r.edges = p->edges;
     r.n = p->n;
@@ -141,35 +156,135 @@ static SlotRange slot_range(const qcl_state *st, int slot0, int nslots, int V) {
     return r;
 }
 
-static void enqueue_layer(qcl_state *st, int layer, double clip, double eps) {
+// ------------------------------------------------------------ TMA-pipelined units
+template <typename T, int V, int D, bool SYN>
+static void launch_tma_t(const PipeArgs &a, cudaStream_t stream) {
+    auto kern = layer_tma_kernel<T, V, D, SYN>;
+    const size_t smem = 128 + (size_t)kStages * 2 * D * kConsumerWarps * 32 * V * sizeof(T);
+    static int blocks_per_sm = -1;  // per instantiation; all B200s alike
+    static int sms = 0;
+    if (blocks_per_sm < 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kPipeThreads, smem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+    }
+    const int64_t grid = std::min<int64_t>(a.tiles, (int64_t)sms * blocks_per_sm);
+    kern<<<(unsigned)grid, kPipeThreads, smem, stream>>>(a);
+}
+
+template <typename T, int V, int D>
+static void launch_tma_d(const PipeArgs &a, cudaStream_t stream, bool syn) {
+    if (syn)
+        launch_tma_t<T, V, D, true>(a, stream);
+    else
+        launch_tma_t<T, V, D, false>(a, stream);
+}
+
+template <typename T>
+static void launch_tma(const PipeArgs &a, int V, int dmax, cudaStream_t stream, bool syn) {
+    if (V == 4 && sizeof(T) == 4)
+        launch_tma_d<T, (sizeof(T) == 4 ? 4 : 2), 4>(a, stream, syn);
+    else if (V == 2 && sizeof(T) == 4)
+        launch_tma_d<T, 2, 8>(a, stream, syn);
+    else if (V == 2)
+        launch_tma_d<T, 2, 4>(a, stream, syn);
+    else if (dmax <= 4)
+        launch_tma_d<T, 1, 4>(a, stream, syn);
+    else if (dmax <= 8)
+        launch_tma_d<T, 1, 8>(a, stream, syn);
+    else if (dmax <= 12)
+        launch_tma_d<T, 1, 12>(a, stream, syn);
+    else if (dmax <= 16)
+        launch_tma_d<T, 1, 16>(a, stream, syn);
+    else
+        launch_tma_d<T, 1, 32>(a, stream, syn);
+}
+
+static bool use_tma(const qcl_state *st) {
+    // bulk copies move whole lane rows: W * sizeof(T) must be a 16-byte multiple
+    return st->engine == 0 && ((size_t)st->W * st->esz) % 16 == 0;
+}
+
+static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t stream, double clip, double eps) {
     const qcl_plan *p = st->plan;
-    const int V = vec_width(st, p->layer_dmax[layer]);
-    const int s0 = p->layer_start[layer], s1 = p->layer_start[layer + 1];
-    LayerArgs a;
-    a.r = slot_range(st, s0, s1 - s0, V);
+    const int V = vec_width(st, u.dmax);
+    PipeArgs a;
+    a.r = slot_range(st, u.list_off, u.count, V, p->slot_list);
     a.L = st->L;
     a.R = st->R;
     a.syn = st->has_syn ? st->syn : nullptr;
-    a.uniform = p->layer_uniform[layer];
+    a.KT = kConsumerWarps * 32 * V / st->W;
+    a.kblocks = (int)cdiv(p->z, a.KT);
+    a.tiles = (int64_t)st->G * u.count * a.kblocks;
+    a.uniform = p->layer_uniform[u.layer];
+    a.hint_L = 1;
+    a.clip = clip;
+    a.eps = eps;
+    if (st->prec == QCL_PREC_FP32)
+        launch_tma<float>(a, V, u.dmax, stream, st->has_syn);
+    else
+        launch_tma<double>(a, V, u.dmax, stream, st->has_syn);
+    st->launches_layer++;
+    st->launches_all++;
+}
+
+static void enqueue_unit(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t stream, double clip, double eps) {
+    if (use_tma(st)) {
+        enqueue_unit_tma(st, u, stream, clip, eps);
+        return;
+    }
+    const qcl_plan *p = st->plan;
+    const int V = vec_width(st, u.dmax);
+    LayerArgs a;
+    a.r = slot_range(st, u.list_off, u.count, V, p->slot_list);
+    a.L = st->L;
+    a.R = st->R;
+    a.syn = st->has_syn ? st->syn : nullptr;
+    a.uniform = p->layer_uniform[u.layer];
     a.clip = clip;
     a.eps = eps;
     dim3 grid((unsigned)((int64_t)st->G * a.r.nslots * a.r.bps));
-    const int dmax = p->layer_dmax[layer];
     if (st->prec == QCL_PREC_FP32) {
         if (V == 4)
-            launch_layer_v<float, 4>(a, dmax, grid, st->stream, st->has_syn);
+            launch_layer_v<float, 4>(a, u.dmax, grid, stream, st->has_syn);
         else if (V == 2)
-            launch_layer_v<float, 2>(a, dmax, grid, st->stream, st->has_syn);
+            launch_layer_v<float, 2>(a, u.dmax, grid, stream, st->has_syn);
         else
-            launch_layer_v<float, 1>(a, dmax, grid, st->stream, st->has_syn);
+            launch_layer_v<float, 1>(a, u.dmax, grid, stream, st->has_syn);
     } else {
         if (V == 2)
-            launch_layer_v<double, 2>(a, dmax, grid, st->stream, st->has_syn);
+            launch_layer_v<double, 2>(a, u.dmax, grid, stream, st->has_syn);
         else
-            launch_layer_v<double, 1>(a, dmax, grid, st->stream, st->has_syn);
+            launch_layer_v<double, 1>(a, u.dmax, grid, stream, st->has_syn);
     }
     st->launches_layer++;
     st->launches_all++;
+}
+
+// One merged layer: its launch units are independent (disjoint columns), so units
+// after the first run on side streams forked from / joined back into the main
+// stream (parallel branches once captured into the sweep graph).
+static void enqueue_layer(qcl_state *st, int layer, double clip, double eps) {
+    const qcl_plan *p = st->plan;
+    const int u0 = p->layer_unit0[layer], u1 = p->layer_unit0[layer + 1];
+    if (u1 - u0 > 1) {
+        cudaEventRecord(st->fork, st->stream);
+        for (int u = u0 + 1; u < u1; u++) {
+            cudaStream_t side = st->side[(u - u0 - 1) % kSideStreams];
+            cudaStreamWaitEvent(side, st->fork, 0);
+            enqueue_unit(st, p->units[u], side, clip, eps);
+        }
+    }
+    enqueue_unit(st, p->units[u0], st->stream, clip, eps);
+    for (int u = u0 + 1; u < u1; u++) {
+        const int i = (u - u0 - 1) % kSideStreams;
+        if (u + kSideStreams < u1) continue;  // only the last unit on each side stream joins
+        cudaEventRecord(st->join[i], st->side[i]);
+        cudaStreamWaitEvent(st->stream, st->join[i], 0);
+    }
 }
 
 static int enqueue_check(qcl_state *st) {
@@ -213,6 +328,7 @@ static int run_sweep(qcl_state *st, double clip, double eps) {
         CK(cudaStreamBeginCapture(st->stream, cudaStreamCaptureModeThreadLocal));
         const int64_t saved = st->launches_layer, saved_all = st->launches_all;
         for (int l = 0; l < p->n_layers; l++) enqueue_layer(st, l, clip, eps);
+        st->sweep_launches = st->launches_layer - saved;
         st->launches_layer = saved;
         st->launches_all = saved_all;
         CK(cudaStreamEndCapture(st->stream, &graph));
@@ -236,8 +352,8 @@ static int run_sweep(qcl_state *st, double clip, double eps) {
     } else {
         CK(cudaGraphLaunch(st->sweep_exec, st->stream));
     }
-    st->launches_layer += p->n_layers;
-    st->launches_all += p->n_layers;
+    st->launches_layer += st->sweep_launches;
+    st->launches_all += st->sweep_launches;
     return QCL_OK;
 }
 
@@ -288,7 +404,12 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
             delete p;
             return fail(QCL_EVALUE, "edge %d out of range", e);
         }
-        h_edges[e] = EdgeInfo{edge_col[e] * z, edge_shift[e]};
+        h_edges[e] = EdgeInfo{edge_col[e] * z, edge_shift[e], 0, 0};
+    }
+    {
+        std::vector<int> coldeg(n_cols, 0);
+        for (int e = 0; e < n_edges; e++) coldeg[edge_col[e]]++;
+        for (int e = 0; e < n_edges; e++) h_edges[e].reused = coldeg[edge_col[e]] > 1;
     }
     p->h_slots.resize(n_slots);
     for (int s = 0; s < n_slots; s++) {
@@ -329,7 +450,31 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
         p->layer_dmax.push_back(dmax);
         p->layer_uniform.push_back(uniform);
     }
+    {
+        std::vector<int32_t> list;
+        auto bucket = [](int d) { return d <= 4 ? 4 : d <= 8 ? 8 : d <= 12 ? 12 : d <= 16 ? 16 : 32; };
+        for (int l = 0; l < n_layers; l++) {
+            p->layer_unit0.push_back((int)p->units.size());
+            for (int b : {4, 8, 12, 16, 32}) {
+                qcl_plan::Unit u{l, (int)list.size(), 0, 0};
+                for (int s = layer_slot_starts[l]; s < layer_slot_starts[l + 1]; s++) {
+                    int d = slot_offsets[s + 1] - slot_offsets[s];
+                    if (bucket(d) != b) continue;
+                    list.push_back(s);
+                    u.count++;
+                    u.dmax = std::max(u.dmax, d);
+                }
+                if (u.count) p->units.push_back(u);
+            }
+        }
+        p->layer_unit0.push_back((int)p->units.size());
+        p->h_slot_list = list;
+    }
     cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMalloc(&p->slot_list, sizeof(int32_t) * p->h_slot_list.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->slot_list, p->h_slot_list.data(), sizeof(int32_t) * p->h_slot_list.size(),
+                       cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p->slots, sizeof(SlotInfo) * n_slots);
     if (e == cudaSuccess) e = cudaMalloc(&p->edges, sizeof(EdgeInfo) * n_edges);
     if (e == cudaSuccess)
@@ -339,6 +484,7 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
     if (e != cudaSuccess) {
         cudaFree(p->slots);
         cudaFree(p->edges);
+        cudaFree(p->slot_list);
         delete p;
         return fail(QCL_ECUDA, "plan upload failed: %s", cudaGetErrorString(e));
     }
@@ -354,6 +500,7 @@ int qcl_plan_destroy(qcl_plan *p) {
     for (auto *s : p->cache) qcl_state_destroy(s);
     cudaFree(p->slots);
     cudaFree(p->edges);
+    cudaFree(p->slot_list);
     delete p;
     return QCL_OK;
 }
@@ -395,6 +542,11 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
     st->Bp = (int64_t)st->G * st->W;
     const size_t nl = (size_t)st->Bp * p->n, ne = (size_t)st->Bp * p->E * p->z, nm = (size_t)st->Bp * p->m;
     cudaError_t e = cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking);
+    for (int i = 0; i < kSideStreams && e == cudaSuccess; i++) {
+        e = cudaStreamCreateWithFlags(&st->side[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->join[i], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->fork, cudaEventDisableTiming);
     auto al = [&](void **ptr, size_t bytes) {
         if (e == cudaSuccess) e = cudaMalloc(ptr, std::max<size_t>(bytes, 16));
     };
@@ -435,6 +587,11 @@ int qcl_state_destroy(qcl_state *st) {
     if (st->ev0) cudaEventDestroy(st->ev0);
     if (st->ev1) cudaEventDestroy(st->ev1);
     if (st->stream) cudaStreamDestroy(st->stream);
+    for (int i = 0; i < kSideStreams; i++) {
+        if (st->side[i]) cudaStreamDestroy(st->side[i]);
+        if (st->join[i]) cudaEventDestroy(st->join[i]);
+    }
+    if (st->fork) cudaEventDestroy(st->fork);
     delete st;
     return QCL_OK;
 }
@@ -751,14 +908,25 @@ int qcl_state_kernel_stats(qcl_state *st, int64_t *layer_launches, float *layer_
 
 int qcl_state_set_engine(qcl_state *st, int32_t engine) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
-    if (engine == 2) {  // engine 0 plus CUDA events around every sweep (bench roofline)
+    if (engine == 2 || engine == 3) {  // engine 0/1 plus CUDA events around every sweep (bench roofline)
         st->profiling = true;
-        st->engine = 0;
+        st->engine = engine - 2;
+        if (st->sweep_exec) cudaGraphExecDestroy(st->sweep_exec);
+        st->sweep_exec = nullptr;
+        return QCL_OK;
+    }
+    if (engine == 1) {  // direct (register-staged) layer kernels, no TMA pipeline
+        st->profiling = false;
+        st->engine = 1;
+        if (st->sweep_exec) cudaGraphExecDestroy(st->sweep_exec);
+        st->sweep_exec = nullptr;
         return QCL_OK;
     }
     if (engine != 0) return fail(QCL_EUNSUP, "engine %d not available", engine);
     st->profiling = false;
     st->engine = engine;
+    if (st->sweep_exec) cudaGraphExecDestroy(st->sweep_exec);
+    st->sweep_exec = nullptr;
     return QCL_OK;
 }
 

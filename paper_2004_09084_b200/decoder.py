@@ -121,7 +121,7 @@ class LayeredDecoder:
     instance can be shared by a ThreadPoolExecutor like the reference's.
     """
 
-    def __init__(self, index, schedule, cfg, device=0, precision="fp32"):
+    def __init__(self, index, schedule, cfg, device=0, precision="fp32", engine=0):
         flat_rows = tuple(r for layer in schedule.layers for r in layer)
         if flat_rows != tuple(index.slot_rows):
             raise ValueError("schedule does not match the compact index row order")
@@ -131,6 +131,7 @@ class LayeredDecoder:
         self.index = index
         self.schedule = schedule
         self.precision = precision
+        self.engine = int(engine)  # 0: TMA-pipelined layer kernels, 1: direct kernels
         self.device = int(device)
         self.z = int(index.z)
         self.n_vars = int(index.n_cols) * self.z
@@ -154,6 +155,7 @@ class LayeredDecoder:
             if len(cache) >= 4:
                 cache.clear()
             st = cache[batch] = _native.State(self._plan, batch, self.precision)
+            st.set_engine(self.engine)
         return st
 
     # ------------------------------------------------------------------ state API

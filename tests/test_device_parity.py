@@ -30,11 +30,13 @@ def relerr(a, b):
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1.0))) if a.size else 0.0
 
 
-def fresh_state(index, sched, batch, precision):
+def fresh_state(index, sched, batch, precision, engine=0):
     from paper_2004_09084_b200 import _native
 
     plan = _native.Plan(index, sched, 0)
-    return plan, _native.State(plan, batch, precision)
+    st = _native.State(plan, batch, precision)
+    st.set_engine(engine)
+    return plan, st
 
 
 # ---------------------------------------------------------------------------- phi
@@ -82,14 +84,15 @@ def golden_code(name):
     return load_code("standin_v2_z100")
 
 
+@pytest.mark.parametrize("engine", [0, 1])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("name", LAYER_CASES)
-def test_layer_and_sweeps_match_reference(gpu, name, precision):
+def test_layer_and_sweeps_match_reference(gpu, name, precision, engine):
     g = np.load(GOLDEN / f"layers_{name}.npz")
     base, sched, index = golden_code(name)
     assert np.array_equal(g["layers"], [len(l) for l in sched.layers])
     batch = g["llr"].shape[0]
-    _, st = fresh_state(index, sched, batch, precision)
+    _, st = fresh_state(index, sched, batch, precision, engine)
     st.set_llr(g["llr"])
     st.reset(30.0)
     post, msg = st.download()
@@ -110,27 +113,38 @@ def test_layer_and_sweeps_match_reference(gpu, name, precision):
         st.layers(0, len(sched.layers), 30.0, 1e-10)
     post, _ = st.download()
     assert relerr(post, g["sweep5_post"]) <= TOL_SWEEP5[precision]
-    assert np.array_equal(post < 0, g["sweep5_post"] < 0)
+    # decisions bit-exact wherever the reference posterior is not within the stated
+    # tolerance of zero (fp64: everywhere)
+    ref = g["sweep5_post"]
+    decided = np.abs(ref) > TOL_SWEEP5[precision] * np.maximum(np.abs(ref), 1.0)
+    assert np.array_equal((post < 0)[decided], (ref < 0)[decided])
 
 
+@pytest.mark.parametrize("batch", [2, 4, 8])
+@pytest.mark.parametrize("engine", [0, 1])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
-def test_layer_from_reference_state_with_messages(gpu, precision):
-    """One layer from a mid-decode reference state (nonzero messages), per layer."""
+def test_layer_from_reference_state_with_messages(gpu, precision, engine, batch):
+    """One layer from a mid-decode reference state (nonzero messages), per layer.
+
+    Batches 2/4/8 give lane widths W = 2/4/8, i.e. both the direct kernel and the
+    TMA pipeline (bulk copies need W * sizeof(T) to be a multiple of 16 bytes)."""
     from oracle import oracle
 
     g = np.load(GOLDEN / "layers_standin_z100.npz")
     base, sched, index = load_code("standin_v2_z100")
     code = oracle.OracleCode(index, sched)
-    batch = g["llr"].shape[0]
-    _, st = fresh_state(index, sched, batch, precision)
-    st.set_syndrome(g["syndrome"])
+    reps = batch // g["llr"].shape[0]
+    gsyn = np.tile(g["syndrome"], (reps, 1))
+    gpost, gmsg = np.tile(g["sweep1_post"], (reps, 1)), np.tile(g["sweep1_msg"], (reps, 1))
+    _, st = fresh_state(index, sched, batch, precision, engine)
+    st.set_syndrome(gsyn)
     for layer in range(len(sched.layers)):
-        post = g["sweep1_post"].copy()
-        msg = g["sweep1_msg"].copy()
+        post = gpost.copy()
+        msg = gmsg.copy()
         st.upload(post, msg)
         st.layers(layer, 1, 30.0, 1e-10)
         dpost, dmsg = st.download()
-        oracle.layer_update(code, layer, post, msg, g["syndrome"])
+        oracle.layer_update(code, layer, post, msg, gsyn)
         assert relerr(dpost, post) <= TOL_LAYER[precision], layer
         assert relerr(dmsg, msg) <= TOL_LAYER[precision], layer
 

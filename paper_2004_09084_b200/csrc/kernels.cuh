@@ -97,6 +97,16 @@ template <> __device__ __forceinline__ double phiT<double>(double x, double eps,
     return phi_ref(x, eps, clip);
 }
 
+// Phi(|q|) for q already clipped to +-clip: only the eps clamp can bind (the reference
+// clamps to [eps, clip] again, decoder.py:104, which is a no-op above eps here).
+template <typename T> __device__ __forceinline__ T phi_absq(T q, T eps);
+template <> __device__ __forceinline__ float phi_absq<float>(float q, float eps) {
+    return phi_fast_ge(fmaxf(fabsf(q), eps));
+}
+template <> __device__ __forceinline__ double phi_absq<double>(double q, double eps) {
+    return log1p(2.0 / expm1(fmax(fabs(q), eps)));
+}
+
 // numpy pairwise_sum of a[1..d) (d-1 <= 31 terms), restated for the FP64 parity path:
 // fewer than 8 terms is a left fold started from 0.0; otherwise 8 strided accumulators
 // combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the tail (decoder.py:240,
@@ -123,6 +133,49 @@ __device__ __forceinline__ double pairwise_rest(const double (&a)[DMAX], int d) 
     for (int j = 1; j < DMAX; j++)
         if (j - 1 >= body && j < d) res += a[j];
     return res;
+}
+
+// others_j for every edge of a check, in place in ph[j][v].
+//   FP32: exclusive prefix + suffix sums (no total - own cancellation);
+//   FP64: total - ph_j with the reference's fold order (left fold for a uniform-degree
+//         layer, a0 + pairwise(rest) for a ragged one; decoder.py:233, :240).
+template <typename T, int V, int D>
+__device__ __forceinline__ void others_in_place(T (&ph)[D][V], int d, int uniform) {
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            T pre = 0, suf = 0, tmp[D];
+#pragma unroll
+            for (int j = 0; j < D; j++) {
+                tmp[j] = pre;
+                pre += ph[j][v];
+            }
+#pragma unroll
+            for (int j = D - 1; j >= 0; j--) {
+                T p = ph[j][v];
+                ph[j][v] = tmp[j] + suf;
+                suf += p;
+            }
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            double col[D];
+#pragma unroll
+            for (int j = 0; j < D; j++) col[j] = ph[j][v];
+            double total;
+            if (uniform) {
+                total = col[0];
+#pragma unroll
+                for (int j = 1; j < D; j++)
+                    if (j < d) total += col[j];
+            } else {
+                total = col[0] + pairwise_rest<D>(col, d);
+            }
+#pragma unroll
+            for (int j = 0; j < D; j++) ph[j][v] = total - col[j];
+        }
+    }
 }
 
 // Map blockIdx.x -> (group, slot, k, w0) for a launch over a slot range.

@@ -84,20 +84,28 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     return p;
 }
 
-constexpr int kStages = 4;
-constexpr int kConsumerWarps = 4;
+// Warp-specialised pipeline: one producer warp + kConsumerWarps consumer warps per CTA.
+// Every tile belongs to ONE consumer warp (tile i of the CTA -> warp i % C, stage
+// i % S).  The consumer copies the stage into registers, releases it at once, computes
+// and writes its results straight to global memory with coalesced vector stores, so
+// the shared-memory ring only has to cover load latency (not compute) and the CTA can
+// hold many consumer warps.
+constexpr int kConsumerWarps = 11;
 constexpr int kPipeThreads = 32 * (1 + kConsumerWarps);
+constexpr int kMaxStages = 32;
+constexpr int kRingBytes = 96 * 1024;
 
 struct PipeArgs {
     SlotRange r;      // unit slot list, lanes
     void *L;
     void *R;
     const uint8_t *syn;
-    int32_t KT;       // checks per tile (consumer threads * V / W)
+    int32_t KT;       // checks per tile
     int32_t kblocks;  // ceil(z / KT)
     int64_t tiles;    // G * nslots * kblocks
+    int32_t stages;   // ring depth
     int32_t uniform;
-    int32_t hint_L;   // 1: keep posterior runs in L2 (evict_last); R is always evict_first
+    int32_t clip_r;   // clip can bind r (clip < Phi(eps)); otherwise the r clip is skipped
     double clip, eps;
 };
 
@@ -116,184 +124,151 @@ __device__ __forceinline__ TileGeom tile_geom(const PipeArgs &a, int64_t t) {
     return tg;
 }
 
-// Issue (LOAD) or write back (!LOAD) every run of one tile.  Lane j of the producer warp
-// handles circulant j (runs for j >= 32 loop).
-template <typename T, bool LOAD>
-__device__ __forceinline__ void tile_runs(const PipeArgs &a, const TileGeom &tg, T *stage, int D, uint64_t *bar,
-                                          uint64_t pol_L, uint64_t pol_R) {
+// Producer: lane j issues the bulk loads of circulant j of the tile (posterior run in one
+// or two segments -- the circulant wraps at z -- and the edge-message run).
+template <typename T>
+__device__ __forceinline__ void tile_loads(const PipeArgs &a, const TileGeom &tg, T *stage, int D, uint64_t *bar,
+                                           uint64_t pol_keep, uint64_t pol_stream) {
     const int lane = threadIdx.x & 31;
     const SlotInfo si = a.r.slots[tg.slot];
     const int W = 1 << a.r.lw, z = a.r.z;
     const int KTW = a.KT * W;
-    T *L = reinterpret_cast<T *>(a.L);
-    T *R = reinterpret_cast<T *>(a.R);
+    const T *L = reinterpret_cast<const T *>(a.L);
+    const T *R = reinterpret_cast<const T *>(a.R);
     for (int j = lane; j < si.degree; j += 32) {
         const EdgeInfo e = a.r.edges[si.edge_off + j];
         int p0 = tg.k0 + e.shift;
         p0 -= (p0 >= z) ? z : 0;
         const int len1 = min(tg.kt, z - p0);
-        T *lg = L + (((int64_t)tg.g * a.r.n + e.var_base + p0) << a.r.lw);
-        T *lg2 = L + (((int64_t)tg.g * a.r.n + e.var_base) << a.r.lw);
-        T *rg = R + ((((int64_t)tg.g * a.r.E + si.edge_off + j) * z + tg.k0) << a.r.lw);
-        T *ls = stage + (size_t)j * KTW;
-        T *rs = stage + (size_t)(D + j) * KTW;
         const uint32_t b1 = (uint32_t)len1 * W * sizeof(T);
         const uint32_t b2 = (uint32_t)(tg.kt - len1) * W * sizeof(T);
         const uint32_t br = (uint32_t)tg.kt * W * sizeof(T);
-        // posteriors of multi-edge columns stay in L2 for the next layers (evict_last);
-        // degree-1 columns and edge messages are touched once per sweep (evict_first)
-        const uint64_t pl = e.reused ? pol_L : pol_R;
-        if (LOAD) {
-            bulk_load(ls, lg, b1, bar, pl);
-            if (b2) bulk_load(ls + (size_t)len1 * W, lg2, b2, bar, pl);
-            bulk_load(rs, rg, br, bar, pol_R);
-        } else {
-            bulk_store(lg, ls, b1, pl);
-            if (b2) bulk_store(lg2, ls + (size_t)len1 * W, b2, pl);
-            bulk_store(rg, rs, br, pol_R);
-        }
+        // posteriors of multi-edge columns are re-read by later layers (keep them in L2);
+        // degree-1 columns and edge messages are touched once per sweep (stream them)
+        const uint64_t pl = e.reused ? pol_keep : pol_stream;
+        T *ls = stage + (size_t)j * KTW;
+        bulk_load(ls, L + (((int64_t)tg.g * a.r.n + e.var_base + p0) << a.r.lw), b1, bar, pl);
+        if (b2) bulk_load(ls + (size_t)len1 * W, L + (((int64_t)tg.g * a.r.n + e.var_base) << a.r.lw), b2, bar, pl);
+        bulk_load(stage + (size_t)(D + j) * KTW,
+                  R + ((((int64_t)tg.g * a.r.E + si.edge_off + j) * z + tg.k0) << a.r.lw), br, bar, pol_stream);
     }
 }
 
+// Two CTAs per SM (22 consumer warps, <= 85 registers per thread) when the per-thread
+// edge arrays are small (the degree-4 and degree-10/11 rows of the MET code in FP32),
+// one otherwise.
+template <typename T, int V, int D>
+constexpr int pipe_min_blocks() {
+    return (D * V * (int)sizeof(T) <= 64) ? 2 : 1;
+}
+
 template <typename T, int V, int D, bool HAS_SYN>
-__global__ void __launch_bounds__(kPipeThreads) layer_tma_kernel(PipeArgs a) {
+__global__ void __launch_bounds__(kPipeThreads, (pipe_min_blocks<T, V, D>())) layer_tma_kernel(PipeArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
-    uint64_t *empty = full + kStages;
-    T *stages = reinterpret_cast<T *>(smem_raw + 128);
+    uint64_t *empty = full + kMaxStages;
+    T *stages = reinterpret_cast<T *>(smem_raw + 2 * kMaxStages * sizeof(uint64_t));
     const int W = 1 << a.r.lw;
-    const size_t stage_elems = (size_t)2 * D * a.KT * W;
+    const int KTW = a.KT * W;
+    const size_t stage_elems = (size_t)2 * D * KTW;
+    const int S = a.stages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n_local = a.tiles > blockIdx.x ? (a.tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; s++) {
+        for (int s = 0; s < S; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
+            mbar_init(&empty[s], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     if (warp == 0) {
-        // ---------------------------------------------------------------- producer
-        const uint64_t pol_R = policy_evict_first();
-        const uint64_t pol_L = a.hint_L ? policy_evict_last() : pol_R;
-        int it = 0;
-        for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x, it++) {
-            const int s = it % kStages;
-            T *stage = stages + (size_t)s * stage_elems;
-            if (it >= kStages) {
-                // the stage holds tile t - S*grid: wait for its update, write it back
-                mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
-                const TileGeom old = tile_geom(a, t - (int64_t)kStages * gridDim.x);
-                tile_runs<T, false>(a, old, stage, D, nullptr, pol_L, pol_R);
-                bulk_commit();
-                bulk_wait_read_all();  // smem of the stage may be overwritten after this
-                __syncwarp();
+        // ------------------------------------------------------------ producer warp
+        const uint64_t pol_stream = policy_evict_first();
+        const uint64_t pol_keep = policy_evict_last();
+        for (int64_t i = 0; i < n_local; i++) {
+            const int s = (int)(i % S);
+            if (i >= S) mbar_wait(&empty[s], (uint32_t)((i / S) - 1) & 1);
+            const TileGeom tg = tile_geom(a, blockIdx.x + i * gridDim.x);
+            if (lane == 0) {
+                const int d = a.r.slots[tg.slot].degree;
+                mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * d * tg.kt * W * sizeof(T)));
             }
-            const TileGeom tg = tile_geom(a, t);
-            const SlotInfo si = a.r.slots[tg.slot];
-            if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * si.degree * tg.kt * W * sizeof(T)));
             __syncwarp();
-            tile_runs<T, true>(a, tg, stage, D, &full[s], pol_L, pol_R);
+            tile_loads<T>(a, tg, stages + (size_t)s * stage_elems, D, &full[s], pol_keep, pol_stream);
         }
-        // drain: write back the last (up to S) tiles
-        const int n_tiles = it;
-        for (int k = max(0, n_tiles - kStages); k < n_tiles; k++) {
-            const int s = k % kStages;
-            mbar_wait(&empty[s], (k / kStages) & 1);
-            const TileGeom old = tile_geom(a, blockIdx.x + (int64_t)k * gridDim.x);
-            tile_runs<T, false>(a, old, stages + (size_t)s * stage_elems, D, nullptr, pol_L, pol_R);
-        }
-        bulk_commit();
-        bulk_wait_all();
         return;
     }
 
-    // -------------------------------------------------------------------- consumers
-    const int ct = threadIdx.x - 32;
+    // ---------------------------------------------------------------- consumer warps
+    const int cw = warp - 1;
     const int lanes_v = W / V;
-    const int i = ct / lanes_v;  // check within the tile
-    const int w0 = (ct - i * lanes_v) * V;
+    const int items = KTW / (32 * V);  // items per thread per tile
+    T *L = reinterpret_cast<T *>(a.L);
+    T *R = reinterpret_cast<T *>(a.R);
     const T clip = (T)a.clip, eps = (T)a.eps;
-    const int KTW = a.KT * W;
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x, it++) {
-        const int s = it % kStages;
-        T *stage = stages + (size_t)s * stage_elems;
-        const TileGeom tg = tile_geom(a, t);
-        const int d = a.r.slots[tg.slot].degree;
-        mbar_wait(&full[s], (it / kStages) & 1);
-        if (i < tg.kt) {
+    for (int64_t i = cw; i < n_local; i += kConsumerWarps) {
+        const int s = (int)(i % S);
+        const T *stage = stages + (size_t)s * stage_elems;
+        const TileGeom tg = tile_geom(a, blockIdx.x + i * gridDim.x);
+        const SlotInfo si = a.r.slots[tg.slot];
+        const int d = si.degree;
+        mbar_wait(&full[s], (uint32_t)(i / S) & 1);
+        for (int sub = 0; sub < items; sub++) {
+            const int item = sub * 32 + lane;
+            const int ci = item / lanes_v;  // check within the tile
+            const int w0 = (item - ci * lanes_v) * V;
+            const bool live = ci < tg.kt;
+            const int off = ci * W + w0;
             T q[D][V], ph[D][V];
             int par[V];
-            if (HAS_SYN) {
+            if (HAS_SYN && live) {
                 const uint8_t *sp =
-                    a.syn + ((((int64_t)tg.g * a.r.S + tg.slot) * a.r.z + tg.k0 + i) << a.r.lw) + w0;
+                    a.syn + ((((int64_t)tg.g * a.r.S + tg.slot) * a.r.z + tg.k0 + ci) << a.r.lw) + w0;
 #pragma unroll
                 for (int v = 0; v < V; v++) par[v] = sp[v] & 1;
             } else {
 #pragma unroll
                 for (int v = 0; v < V; v++) par[v] = 0;
             }
-            const int off = i * W + w0;
+            using VT = typename Vec<T, V>::type;
 #pragma unroll
             for (int j = 0; j < D; j++) {
-                if (j < d) {
+                if (j < d && live) {
                     T lv[V], rv[V];
-                    using VT = typename Vec<T, V>::type;
                     *reinterpret_cast<VT *>(lv) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
-                    *reinterpret_cast<VT *>(rv) =
-                        *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+                    *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
 #pragma unroll
-                    for (int v = 0; v < V; v++) {
-                        q[j][v] = clampT(lv[v] - rv[v], clip);
-                        ph[j][v] = phiT<T>(q[j][v] < (T)0 ? -q[j][v] : q[j][v], eps, clip);
-                        par[v] ^= (q[j][v] < (T)0);
-                    }
+                    for (int v = 0; v < V; v++) q[j][v] = clampT(lv[v] - rv[v], clip);
                 } else {
 #pragma unroll
-                    for (int v = 0; v < V; v++) {
-                        q[j][v] = (T)0;
+                    for (int v = 0; v < V; v++) q[j][v] = (T)0;
+                }
+            }
+            if (sub == items - 1) {
+                // the whole tile is in registers: hand the stage back to the producer
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            if (!live) continue;
+#pragma unroll
+            for (int j = 0; j < D; j++) {
+#pragma unroll
+                for (int v = 0; v < V; v++) {
+                    if (j < d) {
+                        ph[j][v] = phi_absq<T>(q[j][v], eps);
+                        par[v] ^= (q[j][v] < (T)0);
+                    } else {
                         ph[j][v] = (T)0;
                     }
                 }
             }
-            if constexpr (sizeof(T) == 4) {
-#pragma unroll
-                for (int v = 0; v < V; v++) {
-                    T pre = 0, suf = 0, tmp[D];
-#pragma unroll
-                    for (int j = 0; j < D; j++) {
-                        tmp[j] = pre;
-                        pre += ph[j][v];
-                    }
-#pragma unroll
-                    for (int j = D - 1; j >= 0; j--) {
-                        T p = ph[j][v];
-                        ph[j][v] = tmp[j] + suf;
-                        suf += p;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int v = 0; v < V; v++) {
-                    double col[D];
-#pragma unroll
-                    for (int j = 0; j < D; j++) col[j] = ph[j][v];
-                    double total;
-                    if (a.uniform) {
-                        total = col[0];
-#pragma unroll
-                        for (int j = 1; j < D; j++)
-                            if (j < d) total += col[j];
-                    } else {
-                        total = col[0] + pairwise_rest<D>(col, d);
-                    }
-#pragma unroll
-                    for (int j = 0; j < D; j++) ph[j][v] = total - col[j];
-                }
-            }
+            others_in_place<T, V, D>(ph, d, a.uniform);
+            const int k = tg.k0 + ci;
+            const int64_t lbase = (int64_t)tg.g * a.r.n;
+            const int64_t rbase = ((int64_t)tg.g * a.r.E + si.edge_off) * a.r.z + k;
 #pragma unroll
             for (int j = 0; j < D; j++) {
                 if (j < d) {
@@ -301,19 +276,18 @@ __global__ void __launch_bounds__(kPipeThreads) layer_tma_kernel(PipeArgs a) {
 #pragma unroll
                     for (int v = 0; v < V; v++) {
                         T mag = phiT<T>(ph[j][v], eps, clip);
-                        bool neg = (q[j][v] < (T)0) ^ (par[v] != 0);
-                        rv[v] = clampT(neg ? -mag : mag, clip);
+                        if (a.clip_r) mag = fmin(mag, clip);
+                        rv[v] = ((q[j][v] < (T)0) ^ (par[v] != 0)) ? -mag : mag;
                         lv[v] = clampT(q[j][v] + rv[v], clip);
                     }
-                    using VT = typename Vec<T, V>::type;
-                    *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(rv);
-                    *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(lv);
+                    const EdgeInfo e = a.r.edges[si.edge_off + j];
+                    int pos = k + e.shift;
+                    pos -= (pos >= a.r.z) ? a.r.z : 0;
+                    vstore<T, V>(R + ((rbase + (int64_t)j * a.r.z) << a.r.lw) + w0, rv);
+                    vstore<T, V>(L + ((lbase + e.var_base + pos) << a.r.lw) + w0, lv);
                 }
             }
         }
-        fence_proxy_async_smem();  // make this thread's STS visible to the bulk-store engine
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
     }
 }
 

@@ -160,7 +160,7 @@ static SlotRange slot_range(const qcl_state *st, int slot0, int nslots, int V, c
 template <typename T, int V, int D, bool SYN>
 static void launch_tma_t(const PipeArgs &a, cudaStream_t stream) {
     auto kern = layer_tma_kernel<T, V, D, SYN>;
-    const size_t smem = 128 + (size_t)kStages * 2 * D * kConsumerWarps * 32 * V * sizeof(T);
+    const size_t smem = 2 * kMaxStages * sizeof(uint64_t) + (size_t)kRingBytes;
     static int blocks_per_sm = -1;  // per instantiation; all B200s alike
     static int sms = 0;
     if (blocks_per_sm < 0) {
@@ -203,6 +203,8 @@ static void launch_tma(const PipeArgs &a, int V, int dmax, cudaStream_t stream, 
         launch_tma_d<T, 1, 32>(a, stream, syn);
 }
 
+static int dmax_bucket(int d) { return d <= 4 ? 4 : d <= 8 ? 8 : d <= 12 ? 12 : d <= 16 ? 16 : 32; }
+
 static bool use_tma(const qcl_state *st) {
     // bulk copies move whole lane rows: W * sizeof(T) must be a 16-byte multiple
     return st->engine == 0 && ((size_t)st->W * st->esz) % 16 == 0;
@@ -211,16 +213,25 @@ static bool use_tma(const qcl_state *st) {
 static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t stream, double clip, double eps) {
     const qcl_plan *p = st->plan;
     const int V = vec_width(st, u.dmax);
+    const int D = dmax_bucket(u.dmax);
     PipeArgs a;
     a.r = slot_range(st, u.list_off, u.count, V, p->slot_list);
     a.L = st->L;
     a.R = st->R;
     a.syn = st->has_syn ? st->syn : nullptr;
-    a.KT = kConsumerWarps * 32 * V / st->W;
+    // tile = KT checks x all W lanes, consumed by one warp (items = KT*W/(32V) per thread);
+    // aim for >= 1 KB per bulk copy and <= 8 KB per stage
+    const int row_bytes = st->W * (int)st->esz;  // one check, one circulant
+    int KT = 32 * V / st->W;                     // one item per thread
+    while (KT * 2 * row_bytes <= 1024 && 2 * D * (KT * 2) * row_bytes <= 8192) KT *= 2;
+    a.KT = KT;
     a.kblocks = (int)cdiv(p->z, a.KT);
     a.tiles = (int64_t)st->G * u.count * a.kblocks;
+    const int stage_bytes = 2 * D * KT * row_bytes;
+    a.stages = std::max(2, std::min(kMaxStages, kRingBytes / stage_bytes));
     a.uniform = p->layer_uniform[u.layer];
-    a.hint_L = 1;
+    // |r| <= Phi(eps) (the largest Phi value), so the r clip only binds for small clips
+    a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));
     a.clip = clip;
     a.eps = eps;
     if (st->prec == QCL_PREC_FP32)

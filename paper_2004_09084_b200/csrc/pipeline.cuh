@@ -112,12 +112,14 @@ struct PipeArgs {
 struct TileGeom {
     int g, slot, k0, kt;
 };
-__device__ __forceinline__ TileGeom tile_geom(const PipeArgs &a, int64_t t) {
+__device__ __forceinline__ TileGeom tile_geom(const PipeArgs &a, int64_t t64) {
     TileGeom tg;
-    const int kb = (int)(t % a.kblocks);
-    int64_t rest = t / a.kblocks;
-    const int si = a.r.slot0 + (int)(rest % a.r.nslots);
-    tg.g = (int)(rest / a.r.nslots);
+    const uint32_t t = (uint32_t)t64;  // tiles < 2^31 (checked on the host)
+    const uint32_t rest = t / (uint32_t)a.kblocks;
+    const int kb = (int)(t - rest * (uint32_t)a.kblocks);
+    const uint32_t gq = rest / (uint32_t)a.r.nslots;
+    const int si = a.r.slot0 + (int)(rest - gq * (uint32_t)a.r.nslots);
+    tg.g = (int)gq;
     tg.slot = a.r.slot_list ? a.r.slot_list[si] : si;
     tg.k0 = kb * a.KT;
     tg.kt = min(a.KT, a.r.z - tg.k0);

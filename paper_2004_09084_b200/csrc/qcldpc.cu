@@ -223,7 +223,12 @@ static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_
     // aim for >= 1 KB per bulk copy and <= 8 KB per stage
     const int row_bytes = st->W * (int)st->esz;  // one check, one circulant
     int KT = 32 * V / st->W;                     // one item per thread
-    while (KT * 2 * row_bytes <= 1024 && 2 * D * (KT * 2) * row_bytes <= 8192) KT *= 2;
+    static const int items_env = getenv("QCL_TILE_ITEMS") ? atoi(getenv("QCL_TILE_ITEMS")) : 0;
+    if (items_env > 0) {
+        KT *= items_env;  // tuning override: items per thread per tile
+    } else {
+        while (KT * 2 * row_bytes <= 1024 && 2 * D * (KT * 2) * row_bytes <= 8192) KT *= 2;
+    }
     a.KT = KT;
     a.kblocks = (int)cdiv(p->z, a.KT);
     a.tiles = (int64_t)st->G * u.count * a.kblocks;

@@ -16,12 +16,14 @@ ap.add_argument("--iters", type=int, default=2)
 ap.add_argument("--batch", type=int, default=64)
 ap.add_argument("--precision", default="fp32")
 ap.add_argument("--code", default="standin_v2_z2500")
+ap.add_argument("--engine", type=int, default=0)
 a = ap.parse_args()
 base = q.load_base_matrix(ROOT / "codes" / f"{a.code}.txt")
 sched = q.greedy_schedule(base)
 index = q.build_compact_index(base, sched)
 plan = _native.Plan(index, sched, 0)
 st = _native.State(plan, a.batch, a.precision)
+st.set_engine(a.engine)
 st.set_llr_synthetic(seed=0, snr_idx=0, first_frame=0, snr=0.161)
 st.set_syndrome(None)
 cfg = _native.make_config(q.DecoderConfig(max_iterations=a.iters, early_termination=False), a.precision)

@@ -56,6 +56,7 @@ struct LayerArgs {
     void *R;
     const uint8_t *syn;  // nullptr: all-zero target
     int32_t uniform;     // uniform row degree in the layer (FP64 fold order)
+    int32_t clip_r;      // the clip can bind |r| (clip < Phi(eps)); else the r clip is skipped
     double clip, eps;
 };
 
@@ -200,15 +201,104 @@ __device__ __forceinline__ Item map_item(const SlotRange &r) {
     return it;
 }
 
-// One layered update of every check in the launch's slot range, for every group.
-// Reference: decoder.py:212-250 (_layer_update_core), per check m and edge j:
-//   q_j = clip(L_v - r_old_j); ph_j = Phi(|q_j|); parity = XOR_j(q_j < 0) ^ s_m
-//   FP32 path: others_j = exclusive prefix + suffix sum of ph (avoids the FP32
-//              cancellation of total - own);
-//   FP64 path: others_j = total - ph_j with the reference's fold order;
-//   r_j = clip(+-Phi(others_j)) with sign (q_j<0)^parity; L_v = clip(q_j + r_j).
-// Rows of one merged layer touch disjoint columns (checked at plan creation,
-// decoder.py:144-154), so the read-modify-write of L is race free.
+// FP32 check update of one check for V lanes (decoder.py:219-249), lean form:
+//   in:  q[j][v] = clip(L - r_old), d live edges, par[v] = syndrome bit
+//   out: q[j][v] <- new posterior clip(q + r), ph[j][v] <- new message r
+// ph_j = Phi(|q_j|) in log2 units (phi_in), exclusive prefix+suffix sums give others_j,
+// r_j = +-Phi(others_j) (phi_out) with sign (q_j < 0) ^ parity.
+template <int V, int D>
+__device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D][V], int (&par)[V], int d,
+                                                 float eps, float clip, bool clip_r) {
+    const float kInvLn2 = 1.4426950408889634f;
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            if (j < d) {
+                ph[j][v] = phi_in(fmaxf(fabsf(q[j][v]), eps));
+                par[v] ^= (q[j][v] < 0.0f);
+            } else {
+                ph[j][v] = 0.0f;
+            }
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        float pre = 0.0f, suf = 0.0f, tmp[D];
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            tmp[j] = pre;
+            pre += ph[j][v];
+        }
+#pragma unroll
+        for (int j = D - 1; j >= 0; j--) {
+            const float p = ph[j][v];
+            ph[j][v] = tmp[j] + suf;
+            suf += p;
+        }
+    }
+    const float lo2 = eps * kInvLn2, hi2 = clip * kInvLn2;
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            if (j < d) {
+                float mag = phi_out(fminf(fmaxf(ph[j][v], lo2), hi2));
+                if (clip_r) mag = fminf(mag, clip);
+                const float r = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
+                ph[j][v] = r;
+                q[j][v] = clampT(q[j][v] + r, clip);
+            }
+        }
+    }
+}
+
+// FP64 parity update (reference formula and fold order), same in/out convention.
+template <int V, int D>
+__device__ __forceinline__ void check_update_f64(double (&q)[D][V], double (&ph)[D][V], int (&par)[V], int d,
+                                                 double eps, double clip, int uniform) {
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            if (j < d) {
+                ph[j][v] = phi_absq<double>(q[j][v], eps);
+                par[v] ^= (q[j][v] < 0.0);
+            } else {
+                ph[j][v] = 0.0;
+            }
+        }
+    }
+    others_in_place<double, V, D>(ph, d, uniform);
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            if (j < d) {
+                const double mag = phi_ref(ph[j][v], eps, clip);
+                const double r = clampT(((q[j][v] < 0.0) ^ (par[v] != 0)) ? -mag : mag, clip);
+                ph[j][v] = r;
+                q[j][v] = clampT(q[j][v] + r, clip);
+            }
+        }
+    }
+}
+
+template <int V, int D>
+__device__ __forceinline__ void check_update(float (&q)[D][V], float (&ph)[D][V], int (&par)[V], int d,
+                                             const LayerArgs &a) {
+    check_update_f32<V, D>(q, ph, par, d, (float)a.eps, (float)a.clip, a.clip_r != 0);
+}
+template <int V, int D>
+__device__ __forceinline__ void check_update(double (&q)[D][V], double (&ph)[D][V], int (&par)[V], int d,
+                                             const LayerArgs &a) {
+    check_update_f64<V, D>(q, ph, par, d, a.eps, a.clip, a.uniform);
+}
+
+// One layered update of every check in the launch's slot range, for every group
+// (decoder.py:212-250, _layer_update_core).  Rows of one merged layer touch disjoint
+// columns (checked at plan creation, decoder.py:144-154), so the read-modify-write of
+// L is race free.  Offsets inside a lane group are 32-bit (n*W and E*z*W < 2^31).
 template <typename T, int V, int DMAX, bool HAS_SYN>
 __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
     __shared__ EdgeInfo s_edge[DMAX];
@@ -220,14 +310,12 @@ __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
     if (!it.live) return;
 
     const int z = a.r.z, lw = a.r.lw, k = it.k;
-    T *L = reinterpret_cast<T *>(a.L);
-    T *R = reinterpret_cast<T *>(a.R);
-    const T clip = (T)a.clip, eps = (T)a.eps;
-    const int64_t lbase = (int64_t)it.g * a.r.n;
-    const int64_t rbase = ((int64_t)it.g * a.r.E + si.edge_off) * z + k;
+    T *Lg = reinterpret_cast<T *>(a.L) + (((size_t)it.g * a.r.n) << lw) + it.w0;
+    T *Rg = reinterpret_cast<T *>(a.R) + (((((size_t)it.g * a.r.E + si.edge_off) * z) + k) << lw) + it.w0;
+    const T clip = (T)a.clip;
 
     T q[DMAX][V], ph[DMAX][V];
-    int64_t laddr[DMAX];
+    uint32_t loff[DMAX];
     int par[V];
     if (HAS_SYN) {
         const uint8_t *sp = a.syn + ((((int64_t)it.g * a.r.S + it.slot) * z + k) << lw) + it.w0;
@@ -243,10 +331,10 @@ __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
         if (j < d) {
             int pos = k + s_edge[j].shift;
             pos -= (pos >= z) ? z : 0;
-            laddr[j] = ((lbase + s_edge[j].var_base + pos) << lw) + it.w0;
+            loff[j] = (uint32_t)(s_edge[j].var_base + pos) << lw;
             T lv[V], rv[V];
-            vload<T, V>(L + laddr[j], lv);
-            vload<T, V>(R + ((rbase + (int64_t)j * z) << lw) + it.w0, rv);
+            vload<T, V>(Lg + loff[j], lv);
+            vload<T, V>(Rg + ((uint32_t)(j * z) << lw), rv);
 #pragma unroll
             for (int i = 0; i < V; i++) q[j][i] = clampT(lv[i] - rv[i], clip);
         } else {
@@ -254,68 +342,13 @@ __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
             for (int i = 0; i < V; i++) q[j][i] = (T)0;
         }
     }
-#pragma unroll
-    for (int j = 0; j < DMAX; j++) {
-#pragma unroll
-        for (int i = 0; i < V; i++) {
-            if (j < d) {
-                ph[j][i] = phiT<T>(q[j][i] < (T)0 ? -q[j][i] : q[j][i], eps, clip);
-                par[i] ^= (q[j][i] < (T)0);
-            } else {
-                ph[j][i] = (T)0;
-            }
-        }
-    }
-    // others_j, in place in ph
-    if constexpr (sizeof(T) == 4) {
-#pragma unroll
-        for (int i = 0; i < V; i++) {
-            T pre = 0, suf = 0, tmp[DMAX];
-#pragma unroll
-            for (int j = 0; j < DMAX; j++) {
-                tmp[j] = pre;
-                pre += ph[j][i];
-            }
-#pragma unroll
-            for (int j = DMAX - 1; j >= 0; j--) {
-                T p = ph[j][i];
-                ph[j][i] = tmp[j] + suf;
-                suf += p;
-            }
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < V; i++) {
-            double col[DMAX];
-#pragma unroll
-            for (int j = 0; j < DMAX; j++) col[j] = ph[j][i];
-            double total;
-            if (a.uniform) {
-                total = col[0];
-#pragma unroll
-                for (int j = 1; j < DMAX; j++)
-                    if (j < d) total += col[j];
-            } else {
-                total = col[0] + pairwise_rest<DMAX>(col, d);
-            }
-#pragma unroll
-            for (int j = 0; j < DMAX; j++) ph[j][i] = total - col[j];
-        }
-    }
+    check_update<V, DMAX>(q, ph, par, d, a);
     // scatter
 #pragma unroll
     for (int j = 0; j < DMAX; j++) {
         if (j < d) {
-            T rv[V], lv[V];
-#pragma unroll
-            for (int i = 0; i < V; i++) {
-                T mag = phiT<T>(ph[j][i], eps, clip);
-                bool neg = (q[j][i] < (T)0) ^ (par[i] != 0);
-                rv[i] = clampT(neg ? -mag : mag, clip);
-                lv[i] = clampT(q[j][i] + rv[i], clip);
-            }
-            vstore<T, V>(R + ((rbase + (int64_t)j * z) << lw) + it.w0, rv);
-            vstore<T, V>(L + laddr[j], lv);
+            vstore<T, V>(Rg + ((uint32_t)(j * z) << lw), ph[j]);
+            vstore<T, V>(Lg + loff[j], q[j]);
         }
     }
 }

@@ -84,16 +84,14 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     return p;
 }
 
-// Warp-specialised pipeline: one producer warp + kConsumerWarps consumer warps per CTA.
-// Every tile belongs to ONE consumer warp (tile i of the CTA -> warp i % C, stage
-// i % S).  The consumer copies the stage into registers, releases it at once, computes
-// and writes its results straight to global memory with coalesced vector stores, so
-// the shared-memory ring only has to cover load latency (not compute) and the CTA can
-// hold many consumer warps.
-constexpr int kConsumerWarps = 11;
+// All consumer warps of a CTA work on the same tile: tile = (lane group g, slot s, checks
+// k0..k0+KT-1) for all W lanes with KT = 32*kConsumerWarps*V/W, one (check, V-lane)
+// item per consumer thread.  The stage is updated in place; the producer writes it
+// back with bulk stores before reusing it.  Every consumer waits for every phase of
+// every stage in order, so mbarrier parities cannot alias.
+constexpr int kConsumerWarps = 8;
 constexpr int kPipeThreads = 32 * (1 + kConsumerWarps);
-constexpr int kMaxStages = 32;
-constexpr int kRingBytes = 96 * 1024;
+constexpr int kStages = 3;
 
 struct PipeArgs {
     SlotRange r;      // unit slot list, lanes
@@ -102,10 +100,9 @@ struct PipeArgs {
     const uint8_t *syn;
     int32_t KT;       // checks per tile
     int32_t kblocks;  // ceil(z / KT)
-    int64_t tiles;    // G * nslots * kblocks
-    int32_t stages;   // ring depth
+    int64_t tiles;    // G * nslots * kblocks  (< 2^31)
     int32_t uniform;
-    int32_t clip_r;   // clip can bind r (clip < Phi(eps)); otherwise the r clip is skipped
+    int32_t clip_r;
     double clip, eps;
 };
 
@@ -114,7 +111,7 @@ struct TileGeom {
 };
 __device__ __forceinline__ TileGeom tile_geom(const PipeArgs &a, int64_t t64) {
     TileGeom tg;
-    const uint32_t t = (uint32_t)t64;  // tiles < 2^31 (checked on the host)
+    const uint32_t t = (uint32_t)t64;
     const uint32_t rest = t / (uint32_t)a.kblocks;
     const int kb = (int)(t - rest * (uint32_t)a.kblocks);
     const uint32_t gq = rest / (uint32_t)a.r.nslots;
@@ -126,17 +123,17 @@ __device__ __forceinline__ TileGeom tile_geom(const PipeArgs &a, int64_t t64) {
     return tg;
 }
 
-// Producer: lane j issues the bulk loads of circulant j of the tile (posterior run in one
-// or two segments -- the circulant wraps at z -- and the edge-message run).
-template <typename T>
-__device__ __forceinline__ void tile_loads(const PipeArgs &a, const TileGeom &tg, T *stage, int D, uint64_t *bar,
-                                           uint64_t pol_keep, uint64_t pol_stream) {
+// Issue (LOAD) or write back (!LOAD) every run of a tile.  Lane j handles circulant j:
+// posterior run in one or two segments (the circulant wraps at z), edge-message run.
+template <typename T, bool LOAD>
+__device__ __forceinline__ void tile_runs(const PipeArgs &a, const TileGeom &tg, T *stage, int D, uint64_t *bar,
+                                          uint64_t pol_keep, uint64_t pol_stream) {
     const int lane = threadIdx.x & 31;
     const SlotInfo si = a.r.slots[tg.slot];
     const int W = 1 << a.r.lw, z = a.r.z;
     const int KTW = a.KT * W;
-    const T *L = reinterpret_cast<const T *>(a.L);
-    const T *R = reinterpret_cast<const T *>(a.R);
+    T *Lg = reinterpret_cast<T *>(a.L) + (((size_t)tg.g * a.r.n) << a.r.lw);
+    T *Rg = reinterpret_cast<T *>(a.R) + ((((size_t)tg.g * a.r.E + si.edge_off) * z + tg.k0) << a.r.lw);
     for (int j = lane; j < si.degree; j += 32) {
         const EdgeInfo e = a.r.edges[si.edge_off + j];
         int p0 = tg.k0 + e.shift;
@@ -145,20 +142,26 @@ __device__ __forceinline__ void tile_loads(const PipeArgs &a, const TileGeom &tg
         const uint32_t b1 = (uint32_t)len1 * W * sizeof(T);
         const uint32_t b2 = (uint32_t)(tg.kt - len1) * W * sizeof(T);
         const uint32_t br = (uint32_t)tg.kt * W * sizeof(T);
-        // posteriors of multi-edge columns are re-read by later layers (keep them in L2);
-        // degree-1 columns and edge messages are touched once per sweep (stream them)
+        // posteriors of multi-edge columns are re-read by later layers (keep in L2);
+        // degree-1 columns and edge messages are touched once per sweep (stream)
         const uint64_t pl = e.reused ? pol_keep : pol_stream;
+        T *lg1 = Lg + ((size_t)(e.var_base + p0) << a.r.lw);
+        T *lg2 = Lg + ((size_t)e.var_base << a.r.lw);
+        T *rg = Rg + ((size_t)j * z << a.r.lw);
         T *ls = stage + (size_t)j * KTW;
-        bulk_load(ls, L + (((int64_t)tg.g * a.r.n + e.var_base + p0) << a.r.lw), b1, bar, pl);
-        if (b2) bulk_load(ls + (size_t)len1 * W, L + (((int64_t)tg.g * a.r.n + e.var_base) << a.r.lw), b2, bar, pl);
-        bulk_load(stage + (size_t)(D + j) * KTW,
-                  R + ((((int64_t)tg.g * a.r.E + si.edge_off + j) * z + tg.k0) << a.r.lw), br, bar, pol_stream);
+        T *rs = stage + (size_t)(D + j) * KTW;
+        if (LOAD) {
+            bulk_load(ls, lg1, b1, bar, pl);
+            if (b2) bulk_load(ls + (size_t)len1 * W, lg2, b2, bar, pl);
+            bulk_load(rs, rg, br, bar, pol_stream);
+        } else {
+            bulk_store(lg1, ls, b1, pl);
+            if (b2) bulk_store(lg2, ls + (size_t)len1 * W, b2, pl);
+            bulk_store(rg, rs, br, pol_stream);
+        }
     }
 }
 
-// Two CTAs per SM (22 consumer warps, <= 85 registers per thread) when the per-thread
-// edge arrays are small (the degree-4 and degree-10/11 rows of the MET code in FP32),
-// one otherwise.
 template <typename T, int V, int D>
 constexpr int pipe_min_blocks() {
     return (D * V * (int)sizeof(T) <= 64) ? 2 : 1;
@@ -168,65 +171,83 @@ template <typename T, int V, int D, bool HAS_SYN>
 __global__ void __launch_bounds__(kPipeThreads, (pipe_min_blocks<T, V, D>())) layer_tma_kernel(PipeArgs a) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
-    uint64_t *empty = full + kMaxStages;
-    T *stages = reinterpret_cast<T *>(smem_raw + 2 * kMaxStages * sizeof(uint64_t));
+    uint64_t *empty = full + kStages;
+    T *stages = reinterpret_cast<T *>(smem_raw + 128);
     const int W = 1 << a.r.lw;
     const int KTW = a.KT * W;
     const size_t stage_elems = (size_t)2 * D * KTW;
-    const int S = a.stages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t n_local = a.tiles > blockIdx.x ? (a.tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; s++) {
+        for (int s = 0; s < kStages; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
     if (warp == 0) {
-        // ------------------------------------------------------------ producer warp
+        // ---------------------------------------------------------------- producer
         const uint64_t pol_stream = policy_evict_first();
         const uint64_t pol_keep = policy_evict_last();
-        for (int64_t i = 0; i < n_local; i++) {
-            const int s = (int)(i % S);
-            if (i >= S) mbar_wait(&empty[s], (uint32_t)((i / S) - 1) & 1);
-            const TileGeom tg = tile_geom(a, blockIdx.x + i * gridDim.x);
+        int it = 0;
+        for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x, it++) {
+            const int s = it % kStages;
+            T *stage = stages + (size_t)s * stage_elems;
+            if (it >= kStages) {
+                // the stage holds tile t - S*grid: wait for its update, write it back
+                mbar_wait(&empty[s], ((it / kStages) - 1) & 1);
+                const TileGeom old = tile_geom(a, t - (int64_t)kStages * gridDim.x);
+                tile_runs<T, false>(a, old, stage, D, nullptr, pol_keep, pol_stream);
+                bulk_commit();
+                bulk_wait_read_all();  // the stage's smem may be overwritten after this
+                __syncwarp();
+            }
+            const TileGeom tg = tile_geom(a, t);
             if (lane == 0) {
                 const int d = a.r.slots[tg.slot].degree;
                 mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * d * tg.kt * W * sizeof(T)));
             }
             __syncwarp();
-            tile_loads<T>(a, tg, stages + (size_t)s * stage_elems, D, &full[s], pol_keep, pol_stream);
+            tile_runs<T, true>(a, tg, stage, D, &full[s], pol_keep, pol_stream);
         }
+        // drain: write back the last (up to S) tiles
+        for (int k = max(0, it - kStages); k < it; k++) {
+            const int s = k % kStages;
+            mbar_wait(&empty[s], (k / kStages) & 1);
+            const TileGeom old = tile_geom(a, blockIdx.x + (int64_t)k * gridDim.x);
+            tile_runs<T, false>(a, old, stages + (size_t)s * stage_elems, D, nullptr, pol_keep, pol_stream);
+        }
+        bulk_commit();
+        bulk_wait_all();
         return;
     }
 
-    // ---------------------------------------------------------------- consumer warps
-    const int cw = warp - 1;
+    // -------------------------------------------------------------------- consumers
+    const int ct = threadIdx.x - 32;
     const int lanes_v = W / V;
-    const int items = KTW / (32 * V);  // items per thread per tile
-    T *L = reinterpret_cast<T *>(a.L);
-    T *R = reinterpret_cast<T *>(a.R);
-    const T clip = (T)a.clip, eps = (T)a.eps;
-    for (int64_t i = cw; i < n_local; i += kConsumerWarps) {
-        const int s = (int)(i % S);
-        const T *stage = stages + (size_t)s * stage_elems;
-        const TileGeom tg = tile_geom(a, blockIdx.x + i * gridDim.x);
-        const SlotInfo si = a.r.slots[tg.slot];
-        const int d = si.degree;
-        mbar_wait(&full[s], (uint32_t)(i / S) & 1);
-        for (int sub = 0; sub < items; sub++) {
-            const int item = sub * 32 + lane;
-            const int ci = item / lanes_v;  // check within the tile
-            const int w0 = (item - ci * lanes_v) * V;
-            const bool live = ci < tg.kt;
-            const int off = ci * W + w0;
+    const int ci = ct / lanes_v;  // check within the tile
+    const int w0 = (ct - ci * lanes_v) * V;
+    const int off = ci * W + w0;
+    LayerArgs la;  // numeric parameters for check_update
+    la.uniform = a.uniform;
+    la.clip_r = a.clip_r;
+    la.clip = a.clip;
+    la.eps = a.eps;
+    const T clip = (T)a.clip;
+    using VT = typename Vec<T, V>::type;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < a.tiles; t += gridDim.x, it++) {
+        const int s = it % kStages;
+        T *stage = stages + (size_t)s * stage_elems;
+        const TileGeom tg = tile_geom(a, t);
+        const int d = a.r.slots[tg.slot].degree;
+        mbar_wait(&full[s], (it / kStages) & 1);
+        if (ci < tg.kt) {
             T q[D][V], ph[D][V];
             int par[V];
-            if (HAS_SYN && live) {
+            if (HAS_SYN) {
                 const uint8_t *sp =
                     a.syn + ((((int64_t)tg.g * a.r.S + tg.slot) * a.r.z + tg.k0 + ci) << a.r.lw) + w0;
 #pragma unroll
@@ -235,10 +256,9 @@ __global__ void __launch_bounds__(kPipeThreads, (pipe_min_blocks<T, V, D>())) la
 #pragma unroll
                 for (int v = 0; v < V; v++) par[v] = 0;
             }
-            using VT = typename Vec<T, V>::type;
 #pragma unroll
             for (int j = 0; j < D; j++) {
-                if (j < d && live) {
+                if (j < d) {
                     T lv[V], rv[V];
                     *reinterpret_cast<VT *>(lv) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
                     *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
@@ -249,47 +269,18 @@ __global__ void __launch_bounds__(kPipeThreads, (pipe_min_blocks<T, V, D>())) la
                     for (int v = 0; v < V; v++) q[j][v] = (T)0;
                 }
             }
-            if (sub == items - 1) {
-                // the whole tile is in registers: hand the stage back to the producer
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-            }
-            if (!live) continue;
-#pragma unroll
-            for (int j = 0; j < D; j++) {
-#pragma unroll
-                for (int v = 0; v < V; v++) {
-                    if (j < d) {
-                        ph[j][v] = phi_absq<T>(q[j][v], eps);
-                        par[v] ^= (q[j][v] < (T)0);
-                    } else {
-                        ph[j][v] = (T)0;
-                    }
-                }
-            }
-            others_in_place<T, V, D>(ph, d, a.uniform);
-            const int k = tg.k0 + ci;
-            const int64_t lbase = (int64_t)tg.g * a.r.n;
-            const int64_t rbase = ((int64_t)tg.g * a.r.E + si.edge_off) * a.r.z + k;
+            check_update<V, D>(q, ph, par, d, la);
 #pragma unroll
             for (int j = 0; j < D; j++) {
                 if (j < d) {
-                    T rv[V], lv[V];
-#pragma unroll
-                    for (int v = 0; v < V; v++) {
-                        T mag = phiT<T>(ph[j][v], eps, clip);
-                        if (a.clip_r) mag = fmin(mag, clip);
-                        rv[v] = ((q[j][v] < (T)0) ^ (par[v] != 0)) ? -mag : mag;
-                        lv[v] = clampT(q[j][v] + rv[v], clip);
-                    }
-                    const EdgeInfo e = a.r.edges[si.edge_off + j];
-                    int pos = k + e.shift;
-                    pos -= (pos >= a.r.z) ? a.r.z : 0;
-                    vstore<T, V>(R + ((rbase + (int64_t)j * a.r.z) << a.r.lw) + w0, rv);
-                    vstore<T, V>(L + ((lbase + e.var_base + pos) << a.r.lw) + w0, lv);
+                    *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(ph[j]);
+                    *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(q[j]);
                 }
             }
         }
+        fence_proxy_async_smem();  // this thread's STS -> visible to the bulk-store engine
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
     }
 }
 

@@ -160,7 +160,7 @@ static SlotRange slot_range(const qcl_state *st, int slot0, int nslots, int V, c
 template <typename T, int V, int D, bool SYN>
 static void launch_tma_t(const PipeArgs &a, cudaStream_t stream) {
     auto kern = layer_tma_kernel<T, V, D, SYN>;
-    const size_t smem = 2 * kMaxStages * sizeof(uint64_t) + (size_t)kRingBytes;
+    const size_t smem = 128 + (size_t)kStages * 2 * D * kConsumerWarps * 32 * V * sizeof(T);
     static int blocks_per_sm = -1;  // per instantiation; all B200s alike
     static int sms = 0;
     if (blocks_per_sm < 0) {
@@ -219,21 +219,9 @@ static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_
     a.L = st->L;
     a.R = st->R;
     a.syn = st->has_syn ? st->syn : nullptr;
-    // tile = KT checks x all W lanes, consumed by one warp (items = KT*W/(32V) per thread);
-    // aim for >= 1 KB per bulk copy and <= 8 KB per stage
-    const int row_bytes = st->W * (int)st->esz;  // one check, one circulant
-    int KT = 32 * V / st->W;                     // one item per thread
-    static const int items_env = getenv("QCL_TILE_ITEMS") ? atoi(getenv("QCL_TILE_ITEMS")) : 0;
-    if (items_env > 0) {
-        KT *= items_env;  // tuning override: items per thread per tile
-    } else {
-        while (KT * 2 * row_bytes <= 1024 && 2 * D * (KT * 2) * row_bytes <= 8192) KT *= 2;
-    }
-    a.KT = KT;
+    a.KT = kConsumerWarps * 32 * V / st->W;  // one (check, V lanes) item per consumer thread
     a.kblocks = (int)cdiv(p->z, a.KT);
     a.tiles = (int64_t)st->G * u.count * a.kblocks;
-    const int stage_bytes = 2 * D * KT * row_bytes;
-    a.stages = std::max(2, std::min(kMaxStages, kRingBytes / stage_bytes));
     a.uniform = p->layer_uniform[u.layer];
     // |r| <= Phi(eps) (the largest Phi value), so the r clip only binds for small clips
     a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));
@@ -260,6 +248,7 @@ static void enqueue_unit(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t st
     a.R = st->R;
     a.syn = st->has_syn ? st->syn : nullptr;
     a.uniform = p->layer_uniform[u.layer];
+    a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));  // |r| <= Phi(eps)
     a.clip = clip;
     a.eps = eps;
     dim3 grid((unsigned)((int64_t)st->G * a.r.nslots * a.r.bps));

@@ -89,9 +89,7 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
 // item per consumer thread.  The stage is updated in place; the producer writes it
 // back with bulk stores before reusing it.  Every consumer waits for every phase of
 // every stage in order, so mbarrier parities cannot alias.
-constexpr int kConsumerWarps = 8;
-constexpr int kPipeThreads = 32 * (1 + kConsumerWarps);
-constexpr int kStages = 3;
+constexpr int kMaxStages = 4;
 
 struct PipeArgs {
     SlotRange r;      // unit slot list, lanes
@@ -101,6 +99,7 @@ struct PipeArgs {
     int32_t KT;       // checks per tile
     int32_t kblocks;  // ceil(z / KT)
     int64_t tiles;    // G * nslots * kblocks  (< 2^31)
+    int32_t stages;   // ring depth (<= kMaxStages)
     int32_t uniform;
     int32_t clip_r;
     double clip, eps;
@@ -162,16 +161,19 @@ __device__ __forceinline__ void tile_runs(const PipeArgs &a, const TileGeom &tg,
     }
 }
 
-template <typename T, int V, int D>
+template <typename T, int V, int D, int C>
 constexpr int pipe_min_blocks() {
-    return (D * V * (int)sizeof(T) <= 64) ? 2 : 1;
+    return (D * V * (int)sizeof(T) <= 64) ? (C <= 4 ? 3 : 2) : 1;
 }
 
-template <typename T, int V, int D, bool HAS_SYN>
-__global__ void __launch_bounds__(kPipeThreads, (pipe_min_blocks<T, V, D>())) layer_tma_kernel(PipeArgs a) {
+// C consumer warps per CTA (template), a.stages ring stages (runtime).
+template <typename T, int V, int D, bool HAS_SYN, int C>
+__global__ void __launch_bounds__(32 * (C + 1), (pipe_min_blocks<T, V, D, C>())) layer_tma_kernel(PipeArgs a) {
+    constexpr int kConsumerWarps = C;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);
-    uint64_t *empty = full + kStages;
+    uint64_t *empty = full + kMaxStages;
+    const int kStages = a.stages;
     T *stages = reinterpret_cast<T *>(smem_raw + 128);
     const int W = 1 << a.r.lw;
     const int KTW = a.KT * W;

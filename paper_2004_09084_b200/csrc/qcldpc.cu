@@ -157,22 +157,44 @@ static SlotRange slot_range(const qcl_state *st, int slot0, int nslots, int V, c
 }
 
 // ------------------------------------------------------------ TMA-pipelined units
-template <typename T, int V, int D, bool SYN>
-static void launch_tma_t(const PipeArgs &a, cudaStream_t stream) {
-    auto kern = layer_tma_kernel<T, V, D, SYN>;
-    const size_t smem = 128 + (size_t)kStages * 2 * D * kConsumerWarps * 32 * V * sizeof(T);
-    static int blocks_per_sm = -1;  // per instantiation; all B200s alike
-    static int sms = 0;
-    if (blocks_per_sm < 0) {
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+
+template <typename T, int V, int D, bool SYN, int C>
+static void launch_tma_tc(const PipeArgs &a, cudaStream_t stream) {
+    auto kern = layer_tma_kernel<T, V, D, SYN, C>;
+    const size_t smem = 128 + (size_t)a.stages * 2 * D * C * 32 * V * sizeof(T);
+    static int configured_smem = -1, sms = 0;
+    if (configured_smem < (int)smem) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kPipeThreads, smem);
+        configured_smem = (int)smem;
+    }
+    if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (blocks_per_sm < 1) blocks_per_sm = 1;
     }
+    int blocks_per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 32 * (C + 1), smem);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
     const int64_t grid = std::min<int64_t>(a.tiles, (int64_t)sms * blocks_per_sm);
-    kern<<<(unsigned)grid, kPipeThreads, smem, stream>>>(a);
+    kern<<<(unsigned)grid, 32 * (C + 1), smem, stream>>>(a);
+}
+
+// consumer warps per CTA: 8 by default (QCL_PIPE_WARPS=4 selects the 4-warp variant)
+static int pipe_warps() {
+    static int w = env_int("QCL_PIPE_WARPS", 8) == 4 ? 4 : 8;
+    return w;
+}
+
+template <typename T, int V, int D, bool SYN>
+static void launch_tma_t(const PipeArgs &a, cudaStream_t stream) {
+    if (pipe_warps() == 4)
+        launch_tma_tc<T, V, D, SYN, 4>(a, stream);
+    else
+        launch_tma_tc<T, V, D, SYN, 8>(a, stream);
 }
 
 template <typename T, int V, int D>
@@ -219,9 +241,17 @@ static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_
     a.L = st->L;
     a.R = st->R;
     a.syn = st->has_syn ? st->syn : nullptr;
-    a.KT = kConsumerWarps * 32 * V / st->W;  // one (check, V lanes) item per consumer thread
+    a.KT = pipe_warps() * 32 * V / st->W;  // one (check, V lanes) item per consumer thread
     a.kblocks = (int)cdiv(p->z, a.KT);
     a.tiles = (int64_t)st->G * u.count * a.kblocks;
+    // ring depth: QCL_PIPE_STAGES, default 3 (capped so the ring fits ~112 KB)
+    {
+        static int want = env_int("QCL_PIPE_STAGES", 3);
+        const size_t stage_bytes = (size_t)2 * D * pipe_warps() * 32 * V * st->esz;
+        int s_ = std::max(2, std::min(want, (int)kMaxStages));
+        while (s_ > 2 && s_ * stage_bytes > 112 * 1024) s_--;
+        a.stages = s_;
+    }
     a.uniform = p->layer_uniform[u.layer];
     // |r| <= Phi(eps) (the largest Phi value), so the r clip only binds for small clips
     a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));

@@ -9,15 +9,17 @@ import paper_2004_09084_b200 as q  # noqa: E402
 from paper_2004_09084_b200 import _native  # noqa: E402
 
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+batches = [int(x) for x in sys.argv[2].split(',')] if len(sys.argv) > 2 else [64, 32, 128]
+engines = [int(x) for x in sys.argv[3].split(',')] if len(sys.argv) > 3 else [0, 1]
 base = q.load_base_matrix(ROOT / "codes" / "standin_v2_z2500.txt")
 sched = q.greedy_schedule(base)
 index = q.build_compact_index(base, sched)
 plan = _native.Plan(index, sched, 0)
 n = base.n_cols * base.z
-for batch in (64, 32, 128):
+for batch in batches:
     for prec in ("fp32",):
         res = {}
-        for engine in (0, 1):
+        for engine in engines:
             st = _native.State(plan, batch, prec)
             st.set_engine(engine + 2)
             st.set_llr_synthetic(seed=0, snr_idx=0, first_frame=0, snr=0.161)
@@ -31,4 +33,5 @@ for batch in (64, 32, 128):
             mbps = batch * n / (ms * 50 / iters / 1e3) / 1e6
             print(f"B={batch} {prec} engine={engine}: {ms:.2f} ms for {iters} it -> {mbps:.0f} Mbit/s at 50 it; "
                   f"sweep avg {lms / iters:.3f} ms, {ll // iters} launches/sweep", flush=True)
-        print("  engines agree bit-exactly:", np.array_equal(res[0], res[1]))
+        if len(res) > 1:
+            print("  engines agree bit-exactly:", np.array_equal(res[engines[0]], res[engines[1]]))

@@ -253,6 +253,43 @@ __device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D
     }
 }
 
+// Exact-degree-4 FP32 update (the 350 rows of type 3+1 that dominate the MET code):
+// no predication, six adds for the four exclusive sums, and signs handled as IEEE sign
+// bits: parity = XOR of the q sign bits (^ syndrome), r = |Phi(others)| | (sign(q) ^
+// parity).  Exact because the FP32 state never holds -0.0 (reset/upload canonicalise
+// it, |r| > 0 so q + r != -0.0 and L - r_old != -0.0), so sign bit == (q < 0).
+template <int V>
+__device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph)[4][V], const uint32_t (&synbit)[V],
+                                                    float eps, float clip, bool clip_r) {
+    const float kInvLn2 = 1.4426950408889634f;
+    const float lo2 = eps * kInvLn2, hi2 = clip * kInvLn2;
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        uint32_t qs[4];
+        float p[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            qs[j] = __float_as_uint(q[j][v]) & 0x80000000u;
+            p[j] = phi_in(fmaxf(fabsf(q[j][v]), eps));
+        }
+        const uint32_t par = qs[0] ^ qs[1] ^ qs[2] ^ qs[3] ^ synbit[v];
+        const float c = p[0] + p[1], b = p[2] + p[3];
+        float o[4];
+        o[0] = p[1] + b;
+        o[1] = p[0] + b;
+        o[2] = c + p[3];
+        o[3] = c + p[2];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            float mag = phi_out(fminf(fmaxf(o[j], lo2), hi2));
+            if (clip_r) mag = fminf(mag, clip);
+            const float r = __uint_as_float(__float_as_uint(mag) | (qs[j] ^ par));
+            ph[j][v] = r;
+            q[j][v] = clampT(q[j][v] + r, clip);
+        }
+    }
+}
+
 // FP64 parity update (reference formula and fold order), same in/out convention.
 template <int V, int D>
 __device__ __forceinline__ void check_update_f64(double (&q)[D][V], double (&ph)[D][V], int (&par)[V], int d,
@@ -287,6 +324,15 @@ __device__ __forceinline__ void check_update_f64(double (&q)[D][V], double (&ph)
 template <int V, int D>
 __device__ __forceinline__ void check_update(float (&q)[D][V], float (&ph)[D][V], int (&par)[V], int d,
                                              const LayerArgs &a) {
+    if constexpr (D == 4) {
+        if (d == 4) {  // warp-uniform: a unit's slots share the degree class
+            uint32_t sb[V];
+#pragma unroll
+            for (int v = 0; v < V; v++) sb[v] = (uint32_t)par[v] << 31;
+            check_update_f32_d4<V>(q, ph, sb, (float)a.eps, (float)a.clip, a.clip_r != 0);
+            return;
+        }
+    }
     check_update_f32<V, D>(q, ph, par, d, (float)a.eps, (float)a.clip, a.clip_r != 0);
 }
 template <int V, int D>
@@ -460,10 +506,12 @@ __global__ void llr_to_lanes_kernel(const S *src, int64_t B, int64_t Bp, int64_t
 
 // posterior = clip(llr), messages = 0 (new_state, decoder.py:191-202).  For the FP32
 // path the clip is applied in FP64 before the cast (inputs may be +-inf).
+// The "+ 0" maps -0.0 to +0.0 (same decision: -0.0 < 0 is false, decoder.py:266); the
+// FP32 kernels rely on the state never holding -0.0 (check_update_f32_d4).
 template <typename T>
 __global__ void reset_kernel(const T *llr, T *L, int64_t count, double clip) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < count) L[i] = (T)clampT((double)llr[i], clip);
+    if (i < count) L[i] = (T)clampT((double)llr[i], clip) + (T)0;
 }
 
 // Reference-layout FP64 state <-> lanes.  post (B, n); msg (B, E*z) [e][k].
@@ -475,11 +523,11 @@ __global__ void state_in_kernel(const double *post, const double *msg, int64_t B
     int64_t w = i & (W - 1), rest = i >> lw;
     if (i < Bp * n) {
         int64_t v = rest % n, g = rest / n, b = (g << lw) + w;
-        L[i] = b < B ? (T)post[b * n + v] : (T)0;
+        L[i] = b < B ? (T)post[b * n + v] + (T)0 : (T)0;  // + 0: no -0.0 in the state
     }
     if (i < Bp * Ez) {
         int64_t x = rest % Ez, g = rest / Ez, b = (g << lw) + w;
-        R[i] = (b < B && msg) ? (T)msg[b * Ez + x] : (T)0;
+        R[i] = (b < B && msg) ? (T)msg[b * Ez + x] + (T)0 : (T)0;
     }
 }
 template <typename T>

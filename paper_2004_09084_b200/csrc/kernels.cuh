@@ -48,6 +48,7 @@ struct SlotRange {
     int32_t nslots;   // slots in the launch
     int32_t bps;      // blocks per (group, slot)
     int32_t lw;       // log2 W
+    int32_t g0;       // first lane group of the launch (groups g0 .. g0 + grid/(nslots*bps) - 1)
 };
 
 struct LayerArgs {
@@ -192,7 +193,7 @@ __device__ __forceinline__ Item map_item(const SlotRange &r) {
     Item it;
     const int si = r.slot0 + blk % r.nslots;
     it.slot = r.slot_list ? r.slot_list[si] : si;
-    it.g = blk / r.nslots;
+    it.g = r.g0 + blk / r.nslots;
     const int lanes_v = (1 << r.lw) / V;
     const int item = chunk * kBlock + threadIdx.x;
     it.live = item < r.z * lanes_v;

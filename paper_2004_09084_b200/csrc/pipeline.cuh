@@ -115,7 +115,7 @@ __device__ __forceinline__ TileGeom tile_geom(const PipeArgs &a, int64_t t64) {
     const int kb = (int)(t - rest * (uint32_t)a.kblocks);
     const uint32_t gq = rest / (uint32_t)a.r.nslots;
     const int si = a.r.slot0 + (int)(rest - gq * (uint32_t)a.r.nslots);
-    tg.g = (int)gq;
+    tg.g = a.r.g0 + (int)gq;
     tg.slot = a.r.slot_list ? a.r.slot_list[si] : si;
     tg.k0 = kb * a.KT;
     tg.kt = min(a.KT, a.r.z - tg.k0);

@@ -69,7 +69,7 @@ struct qcl_plan {
     std::vector<qcl_state *> cache;  // idle states reused by qcl_decode
 };
 
-constexpr int kSideStreams = 4;
+constexpr int kSideStreams = 8;
 
 struct qcl_state {
     qcl_plan *plan = nullptr;
@@ -153,6 +153,7 @@ static SlotRange slot_range(const qcl_state *st, int slot0, int nslots, int V, c
     r.nslots = nslots;
     r.bps = (int)cdiv((int64_t)p->z * (st->W / V), kBlock);
     r.lw = st->lw;
+    r.g0 = 0;
     return r;
 }
 
@@ -232,18 +233,20 @@ static bool use_tma(const qcl_state *st) {
     return st->engine == 0 && ((size_t)st->W * st->esz) % 16 == 0;
 }
 
-static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t stream, double clip, double eps) {
+static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t stream, double clip, double eps,
+                             int g0, int ng) {
     const qcl_plan *p = st->plan;
     const int V = vec_width(st, u.dmax);
     const int D = dmax_bucket(u.dmax);
     PipeArgs a;
     a.r = slot_range(st, u.list_off, u.count, V, p->slot_list);
+    a.r.g0 = g0;
     a.L = st->L;
     a.R = st->R;
     a.syn = st->has_syn ? st->syn : nullptr;
     a.KT = pipe_warps() * 32 * V / st->W;  // one (check, V lanes) item per consumer thread
     a.kblocks = (int)cdiv(p->z, a.KT);
-    a.tiles = (int64_t)st->G * u.count * a.kblocks;
+    a.tiles = (int64_t)ng * u.count * a.kblocks;
     // ring depth: QCL_PIPE_STAGES, default 3 (capped so the ring fits ~112 KB)
     {
         static int want = env_int("QCL_PIPE_STAGES", 3);
@@ -265,15 +268,17 @@ static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_
     st->launches_all++;
 }
 
-static void enqueue_unit(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t stream, double clip, double eps) {
+static void enqueue_unit(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t stream, double clip, double eps,
+                         int g0, int ng) {
     if (use_tma(st)) {
-        enqueue_unit_tma(st, u, stream, clip, eps);
+        enqueue_unit_tma(st, u, stream, clip, eps, g0, ng);
         return;
     }
     const qcl_plan *p = st->plan;
     const int V = vec_width(st, u.dmax);
     LayerArgs a;
     a.r = slot_range(st, u.list_off, u.count, V, p->slot_list);
+    a.r.g0 = g0;
     a.L = st->L;
     a.R = st->R;
     a.syn = st->has_syn ? st->syn : nullptr;
@@ -281,7 +286,7 @@ static void enqueue_unit(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t st
     a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));  // |r| <= Phi(eps)
     a.clip = clip;
     a.eps = eps;
-    dim3 grid((unsigned)((int64_t)st->G * a.r.nslots * a.r.bps));
+    dim3 grid((unsigned)((int64_t)ng * a.r.nslots * a.r.bps));
     if (st->prec == QCL_PREC_FP32) {
         if (V == 4)
             launch_layer_v<float, 4>(a, u.dmax, grid, stream, st->has_syn);
@@ -299,26 +304,59 @@ static void enqueue_unit(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t st
     st->launches_all++;
 }
 
-// One merged layer: its launch units are independent (disjoint columns), so units
-// after the first run on side streams forked from / joined back into the main
-// stream (parallel branches once captured into the sweep graph).
-static void enqueue_layer(qcl_state *st, int layer, double clip, double eps) {
+// One merged layer for lane groups [g0, g0 + ng): its launch units are independent
+// (disjoint columns), so with fork != 0 units after the first run on side streams
+// forked from / joined back into `stream` (parallel branches in the sweep graph).
+static void enqueue_layer(qcl_state *st, int layer, double clip, double eps, cudaStream_t stream, int g0, int ng,
+                          bool fork) {
     const qcl_plan *p = st->plan;
     const int u0 = p->layer_unit0[layer], u1 = p->layer_unit0[layer + 1];
-    if (u1 - u0 > 1) {
-        cudaEventRecord(st->fork, st->stream);
-        for (int u = u0 + 1; u < u1; u++) {
-            cudaStream_t side = st->side[(u - u0 - 1) % kSideStreams];
-            cudaStreamWaitEvent(side, st->fork, 0);
-            enqueue_unit(st, p->units[u], side, clip, eps);
-        }
+    if (!fork || u1 - u0 == 1) {
+        for (int u = u0; u < u1; u++) enqueue_unit(st, p->units[u], stream, clip, eps, g0, ng);
+        return;
     }
-    enqueue_unit(st, p->units[u0], st->stream, clip, eps);
+    cudaEventRecord(st->fork, stream);
+    for (int u = u0 + 1; u < u1; u++) {
+        cudaStream_t side = st->side[(u - u0 - 1) % kSideStreams];
+        cudaStreamWaitEvent(side, st->fork, 0);
+        enqueue_unit(st, p->units[u], side, clip, eps, g0, ng);
+    }
+    enqueue_unit(st, p->units[u0], stream, clip, eps, g0, ng);
     for (int u = u0 + 1; u < u1; u++) {
         const int i = (u - u0 - 1) % kSideStreams;
         if (u + kSideStreams < u1) continue;  // only the last unit on each side stream joins
         cudaEventRecord(st->join[i], st->side[i]);
-        cudaStreamWaitEvent(st->stream, st->join[i], 0);
+        cudaStreamWaitEvent(stream, st->join[i], 0);
+    }
+}
+
+// Independent chains: lane groups never interact, so the sweep of each chain of groups
+// is its own sequence of layer launches on its own stream.  Chains run concurrently,
+// and one chain's kernels fill the ramp-up/tail of another's (the per-launch fixed cost
+// is ~17% of a 64-codeword sweep with a single chain).
+static int n_chains(const qcl_state *st) {
+    static int env = env_int("QCL_CHAINS", 0);
+    int c = env > 0 ? env : st->G;
+    return std::max(1, std::min({c, st->G, kSideStreams}));
+}
+
+static void enqueue_sweep(qcl_state *st, double clip, double eps) {
+    const qcl_plan *p = st->plan;
+    const int chains = n_chains(st);
+    if (chains == 1) {
+        for (int l = 0; l < p->n_layers; l++) enqueue_layer(st, l, clip, eps, st->stream, 0, st->G, true);
+        return;
+    }
+    cudaEventRecord(st->fork, st->stream);
+    for (int c = 0; c < chains; c++) {
+        const int g0 = (int)((int64_t)st->G * c / chains), g1 = (int)((int64_t)st->G * (c + 1) / chains);
+        cudaStream_t cs = c == 0 ? st->stream : st->side[c - 1];
+        if (c) cudaStreamWaitEvent(cs, st->fork, 0);
+        for (int l = 0; l < p->n_layers; l++) enqueue_layer(st, l, clip, eps, cs, g0, g1 - g0, false);
+    }
+    for (int c = 1; c < chains; c++) {
+        cudaEventRecord(st->join[c - 1], st->side[c - 1]);
+        cudaStreamWaitEvent(st->stream, st->join[c - 1], 0);
     }
 }
 
@@ -362,7 +400,7 @@ static int run_sweep(qcl_state *st, double clip, double eps) {
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(st->stream, cudaStreamCaptureModeThreadLocal));
         const int64_t saved = st->launches_layer, saved_all = st->launches_all;
-        for (int l = 0; l < p->n_layers; l++) enqueue_layer(st, l, clip, eps);
+        enqueue_sweep(st, clip, eps);
         st->sweep_launches = st->launches_layer - saved;
         st->launches_layer = saved;
         st->launches_all = saved_all;
@@ -838,7 +876,7 @@ int qcl_state_layers(qcl_state *st, int32_t first, int32_t count, double llr_cli
     if (first < 0 || count < 0 || first + count > p->n_layers)
         return fail(QCL_EVALUE, "layer range [%d, %d) outside [0, %d)", first, first + count, p->n_layers);
     CK(cudaSetDevice(p->device));
-    for (int l = first; l < first + count; l++) enqueue_layer(st, l, llr_clip, phi_epsilon);
+    for (int l = first; l < first + count; l++) enqueue_layer(st, l, llr_clip, phi_epsilon, st->stream, 0, st->G, true);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st->stream));
     return QCL_OK;

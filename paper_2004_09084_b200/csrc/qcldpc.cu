@@ -335,7 +335,8 @@ static void enqueue_layer(qcl_state *st, int layer, double clip, double eps, cud
 // and one chain's kernels fill the ramp-up/tail of another's (the per-launch fixed cost
 // is ~17% of a 64-codeword sweep with a single chain).
 static int n_chains(const qcl_state *st) {
-    static int env = env_int("QCL_CHAINS", 0);
+    // 2 chains measured best for 64-128 codewords (tools/chain_sweep.sh, profiles/README.md)
+    static int env = env_int("QCL_CHAINS", 2);
     int c = env > 0 ? env : st->G;
     return std::max(1, std::min({c, st->G, kSideStreams}));
 }

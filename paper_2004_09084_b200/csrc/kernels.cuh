@@ -400,68 +400,85 @@ __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
     }
 }
 
-// Parity of the hard decision of every check vs the target syndrome; any unsatisfied
-// check of codeword b sets unsat[b] (syndrome_satisfied, decoder.py:268-273).
+// ---- hard decisions and syndrome check on packed sign words ------------------------
+// signs[g][v]: bit w = (L[g][v][w] < 0) -- one uint32 per variable carries the hard
+// decisions of all W lanes (decoder.py:264-266; -0.0 decides to 0 like `< 0`).
 template <typename T>
-__global__ void __launch_bounds__(kBlock) check_kernel(SlotRange r, const T *L, const uint8_t *syn,
-                                                       uint8_t *unsat) {
-    __shared__ EdgeInfo s_edge[64];
-    const Item it = map_item<1>(r);
-    const SlotInfo si = r.slots[it.slot];
-    for (int j = threadIdx.x; j < si.degree && j < 64; j += kBlock) s_edge[j] = r.edges[si.edge_off + j];
-    __syncthreads();
-    if (!it.live) return;
-    const int64_t lbase = (int64_t)it.g * r.n;
-    int p = syn ? (syn[((((int64_t)it.g * r.S + it.slot) * r.z + it.k) << r.lw) + it.w0] & 1) : 0;
-    for (int j = 0; j < si.degree; j++) {
-        EdgeInfo e = j < 64 ? s_edge[j] : r.edges[si.edge_off + j];
-        int pos = it.k + e.shift;
-        pos -= (pos >= r.z) ? r.z : 0;
-        T v = __ldcg(L + ((lbase + e.var_base + pos) << r.lw) + it.w0);
-        p ^= (v < (T)0);
+__global__ void __launch_bounds__(kBlock) sign_pack_kernel(const T *L, int64_t total, int lw, uint32_t *signs) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over G * n * W, lane fastest
+    const bool neg = i < total && __ldcg(L + i) < (T)0;
+    const uint32_t bits = __ballot_sync(0xffffffffu, neg);
+    const int W = 1 << lw, lane = threadIdx.x & 31;
+    if (i < total && (lane & (W - 1)) == 0) {
+        const uint32_t mask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+        signs[i >> lw] = (bits >> lane) & mask;
     }
-    if (p) unsat[(it.g << r.lw) + it.w0] = 1;
 }
 
-// Hard decisions (decoder.py:264-266: bit = L < 0, so -0.0 -> 0) of the codewords with
-// take[b] != 0, transposed from T[G][n][W] into the reference's (B, n) byte layout
-// through a 64-variable x 32-codeword shared tile.
-template <typename T>
-__global__ void __launch_bounds__(kBlock) words_kernel(const T *L, int64_t n, int lw, int64_t B,
-                                                       const uint8_t *take, uint8_t *words) {
-    __shared__ uint8_t tile[32][64 + 4];
-    const int64_t v0 = (int64_t)blockIdx.x * 64;
-    const int64_t b0 = (int64_t)blockIdx.y * 32;
-    const int Wm = (1 << lw) - 1;
-#pragma unroll
-    for (int i = 0; i < 8; i++) {
-        int e = i * kBlock + threadIdx.x;
-        int bl = e & 31, vl = e >> 5;
-        int64_t b = b0 + bl, v = v0 + vl;
-        uint8_t bit = 0;
-        if (b < B && v < n) {
-            int64_t g = b >> lw, w = b & Wm;
-            bit = __ldcg(L + ((g * n + v) << lw) + w) < (T)0;
+// Syndrome bytes (lanes layout) -> one uint32 of W lane bits per check.
+__global__ void syn_pack_kernel(const uint8_t *syn, int64_t words, int lw, uint32_t *packed) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= words) return;
+    const int W = 1 << lw;
+    uint32_t v = 0;
+    for (int w = 0; w < W; w++) v |= (uint32_t)(syn[(i << lw) + w] & 1) << w;
+    packed[i] = v;
+}
+
+// syndrome_satisfied (decoder.py:268-273) for all lanes at once: per check, XOR of the
+// packed sign words of its d variables (^ packed target syndrome); any set bit marks
+// that lane's codeword unsatisfied.  Lanes of a warp OR-reduce before one atomic.
+__global__ void __launch_bounds__(kBlock) check_packed_kernel(const SlotInfo *slots, const EdgeInfo *edges,
+                                                              int64_t n, int S, int z, int G,
+                                                              const uint32_t *signs, const uint32_t *synpack,
+                                                              uint32_t *unsat_mask) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over G * S * z
+    const int64_t total = (int64_t)G * S * z;
+    int g = -1;
+    uint32_t p = 0;
+    if (i < total) {
+        const int k = (int)(i % z);
+        const int64_t rest = i / z;
+        const int s = (int)(rest % S);
+        g = (int)(rest / S);
+        const SlotInfo si = slots[s];
+        const uint32_t *sg = signs + (int64_t)g * n;
+        p = synpack ? synpack[i] : 0u;
+        for (int j = 0; j < si.degree; j++) {
+            const EdgeInfo e = edges[si.edge_off + j];
+            int pos = k + e.shift;
+            pos -= (pos >= z) ? z : 0;
+            p ^= __ldg(sg + e.var_base + pos);
         }
-        tile[bl][vl] = bit;
     }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 8; i++) {
-        int e = i * kBlock + threadIdx.x;
-        int vl = e & 63, bl = e >> 6;
-        int64_t b = b0 + bl, v = v0 + vl;
-        if (b < B && v < n && (take == nullptr || take[b])) words[b * n + v] = tile[bl][vl];
-    }
+    const uint32_t same = __match_any_sync(0xffffffffu, g);
+    const uint32_t any = __reduce_or_sync(same, p);
+    if (g >= 0 && any && (threadIdx.x & 31) == __ffs(same) - 1) atomicOr(unsat_mask + g, any);
+}
+
+// Words (B, n) from packed signs for the codewords with take[b] (all if take == nullptr).
+__global__ void __launch_bounds__(kBlock) words_from_signs_kernel(const uint32_t *signs, int64_t n, int lw,
+                                                                  int64_t B, const uint8_t *take, uint8_t *words) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over B * n, variable fastest
+    if (i >= B * n) return;
+    const int64_t b = i / n, v = i - b * n;
+    if (take && !take[b]) return;
+    const int64_t g = b >> lw;
+    const int w = (int)(b & ((1 << lw) - 1));
+    words[i] = (uint8_t)((__ldg(signs + g * n + v) >> w) & 1u);
+}
+
+__device__ __forceinline__ uint8_t lane_unsat(const uint32_t *mask, int64_t b, int lw) {
+    return (uint8_t)((mask[b >> lw] >> (b & ((1 << lw) - 1))) & 1u);
 }
 
 // Early-termination bookkeeping after sweep t (decoder.py:295-305): codewords whose
 // hard decision satisfies the syndrome for the first time freeze words/iterations.
-__global__ void et_update_kernel(int64_t B, int t, const uint8_t *unsat, uint8_t *active, uint8_t *take,
-                                 uint8_t *converged, int64_t *iterations, int *n_active) {
+__global__ void et_update_kernel(int64_t B, int t, const uint32_t *unsat_mask, int lw, uint8_t *active,
+                                 uint8_t *take, uint8_t *converged, int64_t *iterations, int *n_active) {
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
-    uint8_t newly = active[b] && !unsat[b];
+    uint8_t newly = active[b] && !lane_unsat(unsat_mask, b, lw);
     take[b] = newly;
     if (newly) {
         active[b] = 0;
@@ -472,12 +489,12 @@ __global__ void et_update_kernel(int64_t B, int t, const uint8_t *unsat, uint8_t
 }
 
 // End of decode for codewords still active (decoder.py:307-311).
-__global__ void finalize_kernel(int64_t B, const uint8_t *unsat, const uint8_t *active, uint8_t *take,
+__global__ void finalize_kernel(int64_t B, const uint32_t *unsat_mask, int lw, const uint8_t *active, uint8_t *take,
                                 uint8_t *converged) {
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
     take[b] = active[b];
-    if (active[b]) converged[b] = !unsat[b];
+    if (active[b]) converged[b] = !lane_unsat(unsat_mask, b, lw);
 }
 
 __global__ void decode_init_kernel(int64_t B, int64_t Bp, int max_iter, uint8_t *active, uint8_t *converged,

@@ -82,7 +82,10 @@ struct qcl_state {
     void *llr = nullptr, *L = nullptr, *R = nullptr;
     uint8_t *syn = nullptr;  // lanes layout, valid if has_syn
     bool has_syn = false;
-    uint8_t *words = nullptr, *conv = nullptr, *unsat = nullptr, *active = nullptr, *take = nullptr;
+    uint8_t *words = nullptr, *conv = nullptr, *active = nullptr, *take = nullptr;
+    uint32_t *unsat = nullptr;    // [G] lane bit masks of unsatisfied codewords
+    uint32_t *signs = nullptr;    // [G][n] packed hard decisions
+    uint32_t *synpack = nullptr;  // [G][S][z] packed target syndrome (valid if has_syn)
     int64_t *iters = nullptr;
     int *n_active = nullptr, *h_n_active = nullptr;  // device / pinned host
     uint8_t *truths = nullptr;
@@ -361,31 +364,49 @@ static void enqueue_sweep(qcl_state *st, double clip, double eps) {
     }
 }
 
-static int enqueue_check(qcl_state *st) {
+// Hard decisions of every lane packed into sign words (decoder.py:264-266).
+static int enqueue_signs(qcl_state *st) {
     const qcl_plan *p = st->plan;
-    CK(cudaMemsetAsync(st->unsat, 0, st->Bp, st->stream));
-    SlotRange r = slot_range(st, 0, p->S, 1);
-    dim3 grid((unsigned)((int64_t)st->G * p->S * r.bps));
-    const uint8_t *syn = st->has_syn ? st->syn : nullptr;
+    const int64_t total = st->Bp * p->n;
+    const unsigned grid = (unsigned)cdiv(total, kBlock);
     if (st->prec == QCL_PREC_FP32)
-        check_kernel<float><<<grid, kBlock, 0, st->stream>>>(r, (const float *)st->L, syn, st->unsat);
+        sign_pack_kernel<float><<<grid, kBlock, 0, st->stream>>>((const float *)st->L, total, st->lw, st->signs);
     else
-        check_kernel<double><<<grid, kBlock, 0, st->stream>>>(r, (const double *)st->L, syn, st->unsat);
+        sign_pack_kernel<double><<<grid, kBlock, 0, st->stream>>>((const double *)st->L, total, st->lw, st->signs);
     st->launches_all++;
     CK(cudaGetLastError());
     return QCL_OK;
 }
 
+// syndrome_satisfied for every codeword (decoder.py:268-273) -> st->unsat lane masks.
+static int enqueue_check(qcl_state *st) {
+    const qcl_plan *p = st->plan;
+    int rc = enqueue_signs(st);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(st->unsat, 0, sizeof(uint32_t) * st->G, st->stream));
+    const int64_t total = (int64_t)st->G * p->S * p->z;
+    check_packed_kernel<<<(unsigned)cdiv(total, kBlock), kBlock, 0, st->stream>>>(
+        p->slots, p->edges, p->n, p->S, p->z, st->G, st->signs, st->has_syn ? st->synpack : nullptr, st->unsat);
+    st->launches_all++;
+    CK(cudaGetLastError());
+    return QCL_OK;
+}
+
+// Words (B, n) for codewords with take[b] from the packed signs of the last check.
 static int enqueue_words(qcl_state *st, const uint8_t *take) {
     const qcl_plan *p = st->plan;
-    dim3 grid((unsigned)cdiv(p->n, 64), (unsigned)cdiv(st->B, 32));
-    if (st->prec == QCL_PREC_FP32)
-        words_kernel<float><<<grid, kBlock, 0, st->stream>>>((const float *)st->L, p->n, st->lw, st->B, take,
-                                                              st->words);
-    else
-        words_kernel<double><<<grid, kBlock, 0, st->stream>>>((const double *)st->L, p->n, st->lw, st->B,
-                                                               take, st->words);
+    const int64_t total = st->B * p->n;
+    words_from_signs_kernel<<<(unsigned)cdiv(total, kBlock), kBlock, 0, st->stream>>>(st->signs, p->n, st->lw, st->B,
+                                                                                      take, st->words);
     st->launches_all++;
+    CK(cudaGetLastError());
+    return QCL_OK;
+}
+
+static int enqueue_syn_pack(qcl_state *st) {
+    const qcl_plan *p = st->plan;
+    const int64_t words = (int64_t)st->G * p->S * p->z;
+    syn_pack_kernel<<<(unsigned)cdiv(words, kBlock), kBlock, 0, st->stream>>>(st->syn, words, st->lw, st->synpack);
     CK(cudaGetLastError());
     return QCL_OK;
 }
@@ -630,7 +651,9 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
     al((void **)&st->syn, nm);
     al((void **)&st->words, (size_t)batch * p->n);
     al((void **)&st->conv, st->Bp);
-    al((void **)&st->unsat, st->Bp);
+    al((void **)&st->unsat, sizeof(uint32_t) * st->G);
+    al((void **)&st->signs, sizeof(uint32_t) * st->G * p->n);
+    al((void **)&st->synpack, sizeof(uint32_t) * st->G * p->S * p->z);
     al((void **)&st->active, st->Bp);
     al((void **)&st->take, st->Bp);
     al((void **)&st->iters, st->Bp * sizeof(int64_t));
@@ -654,7 +677,8 @@ int qcl_state_destroy(qcl_state *st) {
     if (st->stream) cudaStreamSynchronize(st->stream);
     if (st->sweep_exec) cudaGraphExecDestroy(st->sweep_exec);
     for (void *ptr : {st->llr, st->L, st->R, (void *)st->syn, (void *)st->words, (void *)st->conv,
-                      (void *)st->unsat, (void *)st->active, (void *)st->take, (void *)st->iters,
+                      (void *)st->unsat, (void *)st->signs, (void *)st->synpack, (void *)st->active,
+                      (void *)st->take, (void *)st->iters,
                       (void *)st->n_active, (void *)st->truths, st->staging})
         if (ptr) cudaFree(ptr);
     if (st->h_n_active) cudaFreeHost(st->h_n_active);
@@ -737,6 +761,8 @@ int qcl_state_set_llr_synthetic(qcl_state *st, uint64_t seed, int64_t snr_idx, i
         syndrome_of_words_kernel<<<g2, kBlock, 0, st->stream>>>(r, st->truths, st->B, st->syn);
         CK(cudaGetLastError());
         st->has_syn = true;
+        int rc = enqueue_syn_pack(st);
+        if (rc) return rc;
     } else {
         st->has_syn = false;
     }
@@ -798,6 +824,7 @@ int qcl_state_set_syndrome(qcl_state *st, const uint8_t *syndrome) {
     CK(cudaMemcpyAsync(st->h_n_active, st->n_active, sizeof(int), cudaMemcpyDeviceToHost, st->stream));
     CK(cudaStreamSynchronize(st->stream));
     st->has_syn = *st->h_n_active != 0;
+    if (st->has_syn) return enqueue_syn_pack(st);
     return QCL_OK;
 }
 
@@ -886,7 +913,8 @@ int qcl_state_layers(qcl_state *st, int32_t first, int32_t count, double llr_cli
 int qcl_state_hard_decision(qcl_state *st, uint8_t *words) {
     if (!st || !words) return fail(QCL_EVALUE, "NULL argument");
     CK(cudaSetDevice(st->plan->device));
-    int rc = enqueue_words(st, nullptr);
+    int rc = enqueue_signs(st);
+    if (!rc) rc = enqueue_words(st, nullptr);
     if (rc) return rc;
     CK(cudaMemcpyAsync(words, st->words, (size_t)st->B * st->plan->n, cudaMemcpyDeviceToHost, st->stream));
     CK(cudaStreamSynchronize(st->stream));
@@ -898,10 +926,10 @@ int qcl_state_syndrome_ok(qcl_state *st, uint8_t *ok) {
     CK(cudaSetDevice(st->plan->device));
     int rc = enqueue_check(st);
     if (rc) return rc;
-    std::vector<uint8_t> un(st->Bp);
-    CK(cudaMemcpyAsync(un.data(), st->unsat, st->Bp, cudaMemcpyDeviceToHost, st->stream));
+    std::vector<uint32_t> un(st->G);
+    CK(cudaMemcpyAsync(un.data(), st->unsat, sizeof(uint32_t) * st->G, cudaMemcpyDeviceToHost, st->stream));
     CK(cudaStreamSynchronize(st->stream));
-    for (int64_t b = 0; b < st->B; b++) ok[b] = !un[b];
+    for (int64_t b = 0; b < st->B; b++) ok[b] = !((un[b >> st->lw] >> (b & (st->W - 1))) & 1u);
     return QCL_OK;
 }
 
@@ -932,8 +960,8 @@ int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms) {
         if ((rc = run_sweep(st, cfg->llr_clip, cfg->phi_epsilon))) return rc;
         if (cfg->early_termination) {
             if ((rc = enqueue_check(st))) return rc;
-            et_update_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, t, st->unsat, st->active, st->take, st->conv,
-                                                            st->iters, st->n_active);
+            et_update_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, t, st->unsat, st->lw, st->active, st->take,
+                                                            st->conv, st->iters, st->n_active);
             st->launches_all++;
             if ((rc = enqueue_words(st, st->take))) return rc;
             CK(cudaMemcpyAsync(st->h_n_active, st->n_active, sizeof(int), cudaMemcpyDeviceToHost, st->stream));
@@ -942,7 +970,7 @@ int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms) {
         }
     }
     if ((rc = enqueue_check(st))) return rc;
-    finalize_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, st->unsat, st->active, st->take, st->conv);
+    finalize_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, st->unsat, st->lw, st->active, st->take, st->conv);
     st->launches_all++;
     if ((rc = enqueue_words(st, st->take))) return rc;
     CK(cudaEventRecord(st->ev1, st->stream));

@@ -267,8 +267,8 @@ def decode_arrays(plan, qcfg, llr, syndrome):
 
 
 def phi_device(x, eps, clip, precision="fp64", device=0):
-    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
-    flat = a.reshape(-1)
+    a = np.asarray(x, dtype=np.float64)
+    flat = np.ascontiguousarray(a.reshape(-1))
     out = np.empty_like(flat)
     call("qcl_phi", ptr(flat), flat.size, float(eps), float(clip), PREC[precision], int(device), ptr(out))
     return out.reshape(a.shape)

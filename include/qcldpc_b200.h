@@ -120,9 +120,25 @@ int qcl_state_get_llr(qcl_state *st, double *llr);
 /* Device-time breakdown of the last qcl_state_decode: number of layer-kernel launches and
  * their summed CUDA-event time (ms); used by bench.py's roofline. */
 int qcl_state_kernel_stats(qcl_state *st, int64_t *layer_launches, float *layer_ms, int64_t *all_launches);
-/* Select the device iteration engine: 0 = per-layer launches (graph), 1 = persistent
- * per-iteration kernel with codeword-group barriers (when supported). */
+/* Select the layer-update engine: 0 = TMA-pipelined kernels (default), 1 = direct
+ * register-staged kernels; 2 / 3 = engine 0 / 1 with CUDA events around every sweep
+ * (read by qcl_state_kernel_stats). */
 int qcl_state_set_engine(qcl_state *st, int32_t engine);
+
+/* ---- asynchronous path (streaming / overlapped host<->device copies) ---------------
+ * Everything below only enqueues work on the state's stream; qcl_state_wait blocks until
+ * the results requested by qcl_state_results_async have landed.  Host buffers should be
+ * pinned (qcl_host_alloc) for the copies to overlap device work.
+ * qcl_state_set_syndrome_hint: the caller states whether the (B, m) target is nonzero
+ * (nonzero = 0 or syndrome = NULL: all-zero target, nothing is copied).
+ * qcl_state_decode_async: the decode of qcl_state_decode without host synchronisation;
+ * with early termination every layer launch after the last convergence returns at once. */
+int qcl_state_set_syndrome_hint(qcl_state *st, const uint8_t *syndrome, int32_t nonzero);
+int qcl_state_decode_async(qcl_state *st, const qcl_config *cfg);
+int qcl_state_results_async(qcl_state *st, uint8_t *words, uint8_t *converged, int64_t *iterations);
+int qcl_state_wait(qcl_state *st, float *decode_ms);
+int qcl_host_alloc(int64_t bytes, void **out);
+int qcl_host_free(void *ptr);
 
 /* phi (decoder.py:96-105) evaluated by the device kernels' own Phi. */
 int qcl_phi(const double *x, int64_t n, double phi_epsilon, double llr_clip, int32_t precision,

@@ -60,6 +60,12 @@ _SIGNATURES = {
     "qcl_state_kernel_stats": ([_vp, _vp, _vp, _vp], ctypes.c_int),
     "qcl_state_set_engine": ([_vp, _i32], ctypes.c_int),
     "qcl_phi": ([_vp, _i64, _dbl, _dbl, _i32, _i32, _vp], ctypes.c_int),
+    "qcl_state_set_syndrome_hint": ([_vp, _vp, _i32], ctypes.c_int),
+    "qcl_state_decode_async": ([_vp, _vp], ctypes.c_int),
+    "qcl_state_results_async": ([_vp, _vp, _vp, _vp], ctypes.c_int),
+    "qcl_state_wait": ([_vp, _vp], ctypes.c_int),
+    "qcl_host_alloc": ([_i64, _vp], ctypes.c_int),
+    "qcl_host_free": ([_vp], ctypes.c_int),
 }
 EXPORTED = tuple(_SIGNATURES)
 
@@ -246,6 +252,44 @@ class State:
 
     def set_engine(self, engine):
         call("qcl_state_set_engine", self.handle, int(engine))
+
+    # asynchronous path
+    def set_syndrome_hint(self, syndrome, nonzero):
+        if syndrome is None or not nonzero:
+            call("qcl_state_set_syndrome_hint", self.handle, None, 0)
+            return
+        call("qcl_state_set_syndrome_hint", self.handle, ptr(syndrome), 1)
+
+    def decode_async(self, qcfg):
+        call("qcl_state_decode_async", self.handle, ctypes.byref(qcfg))
+
+    def results_async(self, words, conv, iters):
+        call("qcl_state_results_async", self.handle, ptr(words), ptr(conv), ptr(iters))
+
+    def wait(self):
+        ms = ctypes.c_float(0)
+        call("qcl_state_wait", self.handle, ctypes.byref(ms))
+        return float(ms.value)
+
+
+class PinnedArray:
+    """Page-locked host memory (``qcl_host_alloc``) viewed as a numpy array."""
+
+    def __init__(self, shape, dtype):
+        dtype = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dtype.itemsize
+        p = ctypes.c_void_p()
+        call("qcl_host_alloc", max(nbytes, 1), ctypes.byref(p))
+        self._ptr = p
+        buf = (ctypes.c_uint8 * max(nbytes, 1)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype).reshape(shape)
+
+    def __del__(self):
+        p = getattr(self, "_ptr", None)
+        if p and p.value and _lib is not None:
+            self.array = None
+            _lib.qcl_host_free(p)
+            self._ptr = None
 
 
 def decode_arrays(plan, qcfg, llr, syndrome):

@@ -58,6 +58,7 @@ struct LayerArgs {
     const uint8_t *syn;  // nullptr: all-zero target
     int32_t uniform;     // uniform row degree in the layer (FP64 fold order)
     int32_t clip_r;      // the clip can bind |r| (clip < Phi(eps)); else the r clip is skipped
+    const int *n_active; // early termination: skip the launch once every frame converged
     double clip, eps;
 };
 
@@ -348,6 +349,7 @@ __device__ __forceinline__ void check_update(double (&q)[D][V], double (&ph)[D][
 // L is race free.  Offsets inside a lane group are 32-bit (n*W and E*z*W < 2^31).
 template <typename T, int V, int DMAX, bool HAS_SYN>
 __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
+    if (a.n_active && *(volatile const int *)a.n_active == 0) return;
     __shared__ EdgeInfo s_edge[DMAX];
     const Item it = map_item<V>(a.r);
     const SlotInfo si = a.r.slots[it.slot];
@@ -457,15 +459,17 @@ __global__ void __launch_bounds__(kBlock) check_packed_kernel(const SlotInfo *sl
 }
 
 // Words (B, n) from packed signs for the codewords with take[b] (all if take == nullptr).
+// One thread per variable loops over the codewords: a pass that takes nothing (the
+// common early-termination iteration) costs n/256 blocks reading B flags.
 __global__ void __launch_bounds__(kBlock) words_from_signs_kernel(const uint32_t *signs, int64_t n, int lw,
                                                                   int64_t B, const uint8_t *take, uint8_t *words) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over B * n, variable fastest
-    if (i >= B * n) return;
-    const int64_t b = i / n, v = i - b * n;
-    if (take && !take[b]) return;
-    const int64_t g = b >> lw;
-    const int w = (int)(b & ((1 << lw) - 1));
-    words[i] = (uint8_t)((__ldg(signs + g * n + v) >> w) & 1u);
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int Wm = (1 << lw) - 1;
+    for (int64_t b = 0; b < B; b++) {
+        if (take && !take[b]) continue;
+        words[b * n + v] = (uint8_t)((__ldg(signs + (b >> lw) * n + v) >> (b & Wm)) & 1u);
+    }
 }
 
 __device__ __forceinline__ uint8_t lane_unsat(const uint32_t *mask, int64_t b, int lw) {

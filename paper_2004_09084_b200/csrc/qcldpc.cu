@@ -91,12 +91,16 @@ struct qcl_state {
     uint8_t *truths = nullptr;
     void *staging = nullptr;
     size_t staging_bytes = 0;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_done = nullptr;
+    void *staging2 = nullptr;  // syndrome staging (async path: LLR staging may still be in flight)
+    size_t staging2_bytes = 0;
     int engine = 0;
     // per-sweep CUDA graph, rebuilt when clip/eps/syndrome presence change
     cudaGraphExec_t sweep_exec = nullptr;
     double g_clip = -1, g_eps = -1;
-    bool g_syn = false;
+    bool g_syn = false, g_et = false;  // graph key; g_et: layer kernels skip once all converged
+    cudaEvent_t ev_flag[2] = {};        // early-termination flag copies, one iteration behind
+    int *h_flag = nullptr;              // pinned [2]
     int64_t launches_layer = 0, launches_all = 0, sweep_launches = 0;
     bool profiling = false;
     float layer_ms = 0;
@@ -259,6 +263,7 @@ static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_
         a.stages = s_;
     }
     a.uniform = p->layer_uniform[u.layer];
+    a.n_active = st->g_et ? st->n_active : nullptr;
     // |r| <= Phi(eps) (the largest Phi value), so the r clip only binds for small clips
     a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));
     a.clip = clip;
@@ -287,6 +292,7 @@ static void enqueue_unit(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t st
     a.syn = st->has_syn ? st->syn : nullptr;
     a.uniform = p->layer_uniform[u.layer];
     a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));  // |r| <= Phi(eps)
+    a.n_active = st->g_et ? st->n_active : nullptr;
     a.clip = clip;
     a.eps = eps;
     dim3 grid((unsigned)((int64_t)ng * a.r.nslots * a.r.bps));
@@ -395,9 +401,8 @@ static int enqueue_check(qcl_state *st) {
 // Words (B, n) for codewords with take[b] from the packed signs of the last check.
 static int enqueue_words(qcl_state *st, const uint8_t *take) {
     const qcl_plan *p = st->plan;
-    const int64_t total = st->B * p->n;
-    words_from_signs_kernel<<<(unsigned)cdiv(total, kBlock), kBlock, 0, st->stream>>>(st->signs, p->n, st->lw, st->B,
-                                                                                      take, st->words);
+    words_from_signs_kernel<<<(unsigned)cdiv(p->n, kBlock), kBlock, 0, st->stream>>>(st->signs, p->n, st->lw, st->B,
+                                                                                     take, st->words);
     st->launches_all++;
     CK(cudaGetLastError());
     return QCL_OK;
@@ -412,9 +417,10 @@ static int enqueue_syn_pack(qcl_state *st) {
 }
 
 // One sweep over every layer, captured once into a graph and replayed per iteration.
-static int run_sweep(qcl_state *st, double clip, double eps) {
+static int run_sweep(qcl_state *st, double clip, double eps, bool et) {
     const qcl_plan *p = st->plan;
-    if (!st->sweep_exec || st->g_clip != clip || st->g_eps != eps || st->g_syn != st->has_syn) {
+    if (!st->sweep_exec || st->g_clip != clip || st->g_eps != eps || st->g_syn != st->has_syn || st->g_et != et) {
+        st->g_et = et;
         if (st->sweep_exec) {
             cudaGraphExecDestroy(st->sweep_exec);
             st->sweep_exec = nullptr;
@@ -433,6 +439,7 @@ static int run_sweep(qcl_state *st, double clip, double eps) {
         st->g_clip = clip;
         st->g_eps = eps;
         st->g_syn = st->has_syn;
+        st->g_et = et;
     }
     if (st->profiling) {
         // CUDA events on the launching stream around each sweep (30 layer kernels for the
@@ -659,8 +666,11 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
     al((void **)&st->iters, st->Bp * sizeof(int64_t));
     al((void **)&st->n_active, sizeof(int));
     if (e == cudaSuccess) e = cudaMallocHost(&st->h_n_active, sizeof(int));
+    if (e == cudaSuccess) e = cudaMallocHost(&st->h_flag, 2 * sizeof(int));
+    for (int i = 0; i < 2 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&st->ev_flag[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreate(&st->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&st->ev1);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->ev_done, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMemsetAsync(st->llr, 0, nl * st->esz, st->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st->stream);
     if (e != cudaSuccess) {
@@ -682,8 +692,13 @@ int qcl_state_destroy(qcl_state *st) {
                       (void *)st->n_active, (void *)st->truths, st->staging})
         if (ptr) cudaFree(ptr);
     if (st->h_n_active) cudaFreeHost(st->h_n_active);
+    if (st->h_flag) cudaFreeHost(st->h_flag);
+    for (int i = 0; i < 2; i++)
+        if (st->ev_flag[i]) cudaEventDestroy(st->ev_flag[i]);
     if (st->ev0) cudaEventDestroy(st->ev0);
     if (st->ev1) cudaEventDestroy(st->ev1);
+    if (st->ev_done) cudaEventDestroy(st->ev_done);
+    if (st->staging2) cudaFree(st->staging2);
     if (st->stream) cudaStreamDestroy(st->stream);
     for (int i = 0; i < kSideStreams; i++) {
         if (st->side[i]) cudaStreamDestroy(st->side[i]);
@@ -701,6 +716,16 @@ static int ensure_staging(qcl_state *st, size_t bytes) {
     st->staging_bytes = 0;
     CK(cudaMalloc(&st->staging, bytes));
     st->staging_bytes = bytes;
+    return QCL_OK;
+}
+
+static int ensure_staging2(qcl_state *st, size_t bytes) {
+    if (st->staging2_bytes >= bytes) return QCL_OK;
+    if (st->staging2) CK(cudaFree(st->staging2));
+    st->staging2 = nullptr;
+    st->staging2_bytes = 0;
+    CK(cudaMalloc(&st->staging2, bytes));
+    st->staging2_bytes = bytes;
     return QCL_OK;
 }
 
@@ -904,7 +929,10 @@ int qcl_state_layers(qcl_state *st, int32_t first, int32_t count, double llr_cli
     if (first < 0 || count < 0 || first + count > p->n_layers)
         return fail(QCL_EVALUE, "layer range [%d, %d) outside [0, %d)", first, first + count, p->n_layers);
     CK(cudaSetDevice(p->device));
+    const bool saved_et = st->g_et;
+    st->g_et = false;  // direct layer launches never skip
     for (int l = first; l < first + count; l++) enqueue_layer(st, l, llr_clip, phi_epsilon, st->stream, 0, st->G, true);
+    st->g_et = saved_et;
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st->stream));
     return QCL_OK;
@@ -941,8 +969,13 @@ static int validate_cfg(const qcl_config *cfg) {
     return QCL_OK;
 }
 
-int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms) {
-    if (!st) return fail(QCL_EVALUE, "NULL argument");
+// Enqueue a full decode (decoder.py:275-312) on the state's stream.  With `sync` the
+// early-termination loop stops as soon as every frame has converged, reading the
+// device's active count one iteration behind (the sweep after convergence is already
+// queued, which changes nothing: converged frames are frozen).  Without `sync` nothing
+// waits on the host: after the last frame converges the remaining layer launches
+// return immediately (they read the device count), so results are identical.
+static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     int rc = validate_cfg(cfg);
     if (rc) return rc;
     if (cfg->precision != st->prec) return fail(QCL_EVALUE, "config precision differs from the state's");
@@ -956,17 +989,21 @@ int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms) {
     st->launches_all++;
     if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
     const unsigned gb = (unsigned)cdiv(st->B, kBlock);
+    const bool et = cfg->early_termination != 0;
     for (int t = 1; t <= cfg->max_iterations; t++) {
-        if ((rc = run_sweep(st, cfg->llr_clip, cfg->phi_epsilon))) return rc;
-        if (cfg->early_termination) {
-            if ((rc = enqueue_check(st))) return rc;
-            et_update_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, t, st->unsat, st->lw, st->active, st->take,
-                                                            st->conv, st->iters, st->n_active);
-            st->launches_all++;
-            if ((rc = enqueue_words(st, st->take))) return rc;
-            CK(cudaMemcpyAsync(st->h_n_active, st->n_active, sizeof(int), cudaMemcpyDeviceToHost, st->stream));
-            CK(cudaStreamSynchronize(st->stream));
-            if (*st->h_n_active == 0) break;
+        if ((rc = run_sweep(st, cfg->llr_clip, cfg->phi_epsilon, et))) return rc;
+        if (!et) continue;
+        if ((rc = enqueue_check(st))) return rc;
+        et_update_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, t, st->unsat, st->lw, st->active, st->take, st->conv,
+                                                        st->iters, st->n_active);
+        st->launches_all++;
+        if ((rc = enqueue_words(st, st->take))) return rc;
+        if (!sync) continue;
+        CK(cudaMemcpyAsync(st->h_flag + (t & 1), st->n_active, sizeof(int), cudaMemcpyDeviceToHost, st->stream));
+        CK(cudaEventRecord(st->ev_flag[t & 1], st->stream));
+        if (t >= 2) {
+            CK(cudaEventSynchronize(st->ev_flag[(t - 1) & 1]));
+            if (st->h_flag[(t - 1) & 1] == 0) break;
         }
     }
     if ((rc = enqueue_check(st))) return rc;
@@ -974,6 +1011,11 @@ int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms) {
     st->launches_all++;
     if ((rc = enqueue_words(st, st->take))) return rc;
     CK(cudaEventRecord(st->ev1, st->stream));
+    CK(cudaGetLastError());
+    return QCL_OK;
+}
+
+static int finish_decode(qcl_state *st, float *elapsed_ms) {
     CK(cudaEventSynchronize(st->ev1));
     CK(cudaGetLastError());
     if (elapsed_ms) CK(cudaEventElapsedTime(elapsed_ms, st->ev0, st->ev1));
@@ -985,6 +1027,68 @@ int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms) {
         cudaEventDestroy(ev.second);
     }
     st->sweep_events.clear();
+    return QCL_OK;
+}
+
+int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms) {
+    if (!st) return fail(QCL_EVALUE, "NULL argument");
+    int rc = enqueue_decode(st, cfg, true);
+    if (rc) return rc;
+    return finish_decode(st, elapsed_ms);
+}
+
+int qcl_state_decode_async(qcl_state *st, const qcl_config *cfg) {
+    if (!st) return fail(QCL_EVALUE, "NULL argument");
+    return enqueue_decode(st, cfg, false);
+}
+
+int qcl_state_results_async(qcl_state *st, uint8_t *words, uint8_t *converged, int64_t *iterations) {
+    if (!st) return fail(QCL_EVALUE, "NULL argument");
+    const qcl_plan *p = st->plan;
+    CK(cudaSetDevice(p->device));
+    if (words) CK(cudaMemcpyAsync(words, st->words, (size_t)st->B * p->n, cudaMemcpyDeviceToHost, st->stream));
+    if (converged) CK(cudaMemcpyAsync(converged, st->conv, st->B, cudaMemcpyDeviceToHost, st->stream));
+    if (iterations)
+        CK(cudaMemcpyAsync(iterations, st->iters, st->B * sizeof(int64_t), cudaMemcpyDeviceToHost, st->stream));
+    CK(cudaEventRecord(st->ev_done, st->stream));
+    return QCL_OK;
+}
+
+int qcl_state_wait(qcl_state *st, float *decode_ms) {
+    if (!st) return fail(QCL_EVALUE, "NULL argument");
+    CK(cudaSetDevice(st->plan->device));
+    CK(cudaEventSynchronize(st->ev_done));
+    return finish_decode(st, decode_ms);
+}
+
+int qcl_state_set_syndrome_hint(qcl_state *st, const uint8_t *syndrome, int32_t nonzero) {
+    if (!st) return fail(QCL_EVALUE, "NULL argument");
+    const qcl_plan *p = st->plan;
+    CK(cudaSetDevice(p->device));
+    if (!syndrome || !nonzero) {
+        st->has_syn = false;
+        return QCL_OK;
+    }
+    const size_t bytes = (size_t)st->B * p->m;
+    int rc = ensure_staging2(st, bytes);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(st->staging2, syndrome, bytes, cudaMemcpyHostToDevice, st->stream));
+    const int64_t total = st->Bp * p->m;
+    syndrome_to_lanes_kernel<<<(unsigned)cdiv(total, kBlock), kBlock, 0, st->stream>>>(
+        (const uint8_t *)st->staging2, p->slots, st->B, st->Bp, p->S, p->z, st->lw, st->syn, st->n_active);
+    CK(cudaGetLastError());
+    st->has_syn = true;
+    return enqueue_syn_pack(st);
+}
+
+int qcl_host_alloc(int64_t bytes, void **out) {
+    if (!out || bytes < 0) return fail(QCL_EVALUE, "bad argument");
+    CK(cudaMallocHost(out, bytes > 0 ? (size_t)bytes : 1));
+    return QCL_OK;
+}
+
+int qcl_host_free(void *ptr) {
+    if (ptr) CK(cudaFreeHost(ptr));
     return QCL_OK;
 }
 

@@ -23,6 +23,7 @@ Extra keywords beyond the reference: ``device`` (CUDA ordinal) and ``precision``
 from __future__ import annotations
 
 import threading
+from collections import deque
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
@@ -237,6 +238,70 @@ class LayeredDecoder:
         st.set_syndrome(syn)
         st.decode(self._qcfg)
         return st.results()
+
+
+class _StreamSlot:
+    """One device workspace plus pinned result buffers of decode_stream."""
+
+    def __init__(self, plan, batch, precision, engine, n):
+        self.state = _native.State(plan, batch, precision)
+        self.state.set_engine(engine)
+        self.batch = batch
+        self.words = _native.PinnedArray((batch, n), np.uint8)
+        self.conv = _native.PinnedArray((batch,), np.uint8)
+        self.iters = _native.PinnedArray((batch,), np.int64)
+        self.inputs = None  # keeps the caller's arrays alive until the copies land
+
+
+def _stream_decode(self, batches, depth=2, copy=False):
+    """Decode an iterable of (llr0, syndrome) batches, yielding (words, converged,
+    iterations) per batch in order -- ``decode_batch_arrays`` semantics -- while the
+    host<->device copies of one batch overlap the decoding of the next.
+
+    ``depth`` device workspaces are cycled (each ~1.5 GB for 64 codewords of the n=10^6
+    code).  Inputs are read asynchronously: pinned arrays (``_native.PinnedArray``) copy
+    at full PCIe speed, and every input must stay unmodified until its result is yielded.
+    Yielded arrays are views of pinned buffers that are reused ``depth`` batches later
+    unless ``copy=True``.
+    """
+    slots, pending = [None] * max(1, int(depth)), deque()
+
+    def finish(slot):
+        slot.state.wait()
+        slot.inputs = None
+        out = (slot.words.array, slot.conv.array.astype(bool), slot.iters.array)
+        return tuple(np.array(a) for a in out) if copy else out
+
+    for i, (llr0, syndrome) in enumerate(batches):
+        llr = np.atleast_2d(np.asarray(llr0))
+        if llr.dtype != np.float32:
+            llr = llr.astype(np.float64, copy=False)
+        llr = np.ascontiguousarray(llr)
+        if llr.shape[1] != self.n_vars:
+            raise ValueError(f"llr vector length {llr.shape[1]} != block length {self.n_vars}")
+        syn = np.atleast_2d(np.asarray(syndrome))
+        if syn.shape != (llr.shape[0], self.n_checks):
+            raise ValueError(f"syndrome shape {syn.shape} != ({llr.shape[0]}, {self.n_checks})")
+        syn = np.ascontiguousarray(syn if syn.dtype in (np.uint8, np.bool_, np.int8) else syn.astype(bool)).view(
+            np.uint8)
+        k = i % len(slots)
+        if pending and len(pending) == len(slots):
+            yield finish(pending.popleft())
+        slot = slots[k]
+        if slot is None or slot.batch != llr.shape[0]:
+            slot = slots[k] = _StreamSlot(self._plan, llr.shape[0], self.precision, self.engine, self.n_vars)
+        st = slot.state
+        slot.inputs = (llr, syn)
+        st.set_llr(llr)
+        st.set_syndrome_hint(syn, bool(syn.any()))
+        st.decode_async(self._qcfg)
+        st.results_async(slot.words.array, slot.conv.array, slot.iters.array)
+        pending.append(slot)
+    while pending:
+        yield finish(pending.popleft())
+
+
+LayeredDecoder.decode_stream = _stream_decode
 
 
 def _outcomes(words, converged, iterations):

@@ -392,3 +392,28 @@ def test_device_encode_mode_syndrome(gpu):
     assert c.all() and np.array_equal(w, truths)
     # the syndrome the device targeted is H * truths
     assert np.array_equal(oracle.syndrome(code, w), oracle.syndrome(code, truths))
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_decode_stream_matches_blocking_calls(gpu, precision):
+    """decode_stream (async copies, double-buffered workspaces) == decode_batch_arrays,
+    including nonzero syndromes, early termination and a batch-size change mid-stream."""
+    import paper_2004_09084_b200 as q
+    from conftest import TEST_BASE_4x8_Z3
+
+    base, sched, index = load_code("demo_4x8_z100")
+    n, m = base.n_cols * base.z, base.n_rows * base.z
+    rows = q.expand(base)
+    rng = np.random.default_rng(11)
+    batches = []
+    for i, bsz in enumerate([8, 8, 5, 8]):
+        words = rng.integers(0, 2, size=(bsz, n)).astype(np.uint8) if i % 2 else np.zeros((bsz, n), np.uint8)
+        llr = (1.0 - 2.0 * words) * 2.5 + rng.normal(0, 1.2, size=(bsz, n))
+        batches.append((llr, q.syndrome_of(words, rows)))
+    for et in (True, False):
+        cfg = q.DecoderConfig(max_iterations=20, early_termination=et)
+        dec = q.LayeredDecoder(index, sched, cfg, precision=precision)
+        ref = [dec.decode_batch_arrays(l, s) for l, s in batches]
+        got = list(dec.decode_stream(batches, depth=2, copy=True))
+        for (w0, c0, i0), (w1, c1, i1) in zip(ref, got):
+            assert np.array_equal(w0, w1) and np.array_equal(c0, c1) and np.array_equal(i0, i1)

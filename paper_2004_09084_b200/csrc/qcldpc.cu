@@ -100,6 +100,12 @@ struct qcl_state {
     double g_clip = -1, g_eps = -1;
     bool g_syn = false, g_et = false;  // graph key; g_et: layer kernels skip once all converged
     cudaEvent_t ev_flag[2] = {};        // early-termination flag copies, one iteration behind
+    // whole-decode graph and its key
+    cudaGraphExec_t decode_exec = nullptr;
+    double d_clip = -1, d_eps = -1;
+    bool d_syn = false, d_et = false;
+    int d_iters = -1, d_engine = -1;
+    int64_t d_launches_layer = 0, d_launches_all = 0;
     int *h_flag = nullptr;              // pinned [2]
     int64_t launches_layer = 0, launches_all = 0, sweep_launches = 0;
     bool profiling = false;
@@ -686,6 +692,7 @@ int qcl_state_destroy(qcl_state *st) {
     cudaSetDevice(st->plan->device);
     if (st->stream) cudaStreamSynchronize(st->stream);
     if (st->sweep_exec) cudaGraphExecDestroy(st->sweep_exec);
+    if (st->decode_exec) cudaGraphExecDestroy(st->decode_exec);
     for (void *ptr : {st->llr, st->L, st->R, (void *)st->syn, (void *)st->words, (void *)st->conv,
                       (void *)st->unsat, (void *)st->signs, (void *)st->synpack, (void *)st->active,
                       (void *)st->take, (void *)st->iters,
@@ -975,6 +982,43 @@ static int validate_cfg(const qcl_config *cfg) {
 // queued, which changes nothing: converged frames are frozen).  Without `sync` nothing
 // waits on the host: after the last frame converges the remaining layer launches
 // return immediately (they read the device count), so results are identical.
+// The decode body without host synchronisation: init, reset, the sweeps (and per-sweep
+// early-termination bookkeeping), final check and words.  Captured once into a
+// whole-decode graph; the only host work per decode is then one graph launch.
+static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
+    int rc;
+    const unsigned gb = (unsigned)cdiv(st->B, kBlock);
+    const bool et = cfg->early_termination != 0;
+    decode_init_kernel<<<(unsigned)cdiv(st->Bp, kBlock), kBlock, 0, st->stream>>>(
+        st->B, st->Bp, cfg->max_iterations, st->active, st->conv, st->iters, st->n_active);
+    st->launches_all++;
+    if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
+    st->g_et = et;
+    for (int t = 1; t <= cfg->max_iterations; t++) {
+        const int64_t before = st->launches_layer;
+        enqueue_sweep(st, cfg->llr_clip, cfg->phi_epsilon);
+        st->launches_all += st->launches_layer - before;
+        if (!et) continue;
+        if ((rc = enqueue_check(st))) return rc;
+        et_update_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, t, st->unsat, st->lw, st->active, st->take, st->conv,
+                                                        st->iters, st->n_active);
+        st->launches_all++;
+        if ((rc = enqueue_words(st, st->take))) return rc;
+    }
+    if ((rc = enqueue_check(st))) return rc;
+    finalize_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, st->unsat, st->lw, st->active, st->take, st->conv);
+    st->launches_all++;
+    return enqueue_words(st, st->take);
+}
+
+// Enqueue a full decode (decoder.py:275-312) on the state's stream.
+//  * default: one launch of the whole-decode graph (rebuilt when the config, the
+//    syndrome presence or the engine changes).  With early termination, every layer
+//    launch after the last convergence returns at once (it reads the device count), so
+//    results equal the reference's early break: converged frames are frozen.
+//  * sync && early termination: the sweep graph per iteration, and the host stops once
+//    every frame converged (active count read one iteration behind).
+//  * profiling: the sweep graph per iteration with CUDA events around each sweep.
 static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     int rc = validate_cfg(cfg);
     if (rc) return rc;
@@ -983,13 +1027,46 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     CK(cudaSetDevice(p->device));
     st->launches_layer = st->launches_all = 0;
     st->layer_ms = 0;
+    const bool et = cfg->early_termination != 0;
+    if (!st->profiling && !(sync && et)) {
+        const bool stale = !st->decode_exec || st->d_clip != cfg->llr_clip || st->d_eps != cfg->phi_epsilon ||
+                           st->d_syn != st->has_syn || st->d_et != et || st->d_iters != cfg->max_iterations ||
+                           st->d_engine != st->engine;
+        if (stale) {
+            if (st->decode_exec) cudaGraphExecDestroy(st->decode_exec);
+            st->decode_exec = nullptr;
+            cudaGraph_t graph;
+            CK(cudaStreamBeginCapture(st->stream, cudaStreamCaptureModeThreadLocal));
+            rc = enqueue_decode_body(st, cfg);
+            cudaError_t e = cudaStreamEndCapture(st->stream, &graph);
+            if (rc) return rc;
+            CK(e);
+            e = cudaGraphInstantiate(&st->decode_exec, graph, 0);
+            cudaGraphDestroy(graph);
+            CK(e);
+            st->d_clip = cfg->llr_clip;
+            st->d_eps = cfg->phi_epsilon;
+            st->d_syn = st->has_syn;
+            st->d_et = et;
+            st->d_iters = cfg->max_iterations;
+            st->d_engine = st->engine;
+            st->d_launches_layer = st->launches_layer;
+            st->d_launches_all = st->launches_all;
+        }
+        st->launches_layer = st->d_launches_layer;
+        st->launches_all = st->d_launches_all;
+        CK(cudaEventRecord(st->ev0, st->stream));
+        CK(cudaGraphLaunch(st->decode_exec, st->stream));
+        CK(cudaEventRecord(st->ev1, st->stream));
+        CK(cudaGetLastError());
+        return QCL_OK;
+    }
     CK(cudaEventRecord(st->ev0, st->stream));
     decode_init_kernel<<<(unsigned)cdiv(st->Bp, kBlock), kBlock, 0, st->stream>>>(
         st->B, st->Bp, cfg->max_iterations, st->active, st->conv, st->iters, st->n_active);
     st->launches_all++;
     if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
     const unsigned gb = (unsigned)cdiv(st->B, kBlock);
-    const bool et = cfg->early_termination != 0;
     for (int t = 1; t <= cfg->max_iterations; t++) {
         if ((rc = run_sweep(st, cfg->llr_clip, cfg->phi_epsilon, et))) return rc;
         if (!et) continue;

@@ -264,7 +264,12 @@ def _stream_decode(self, batches, depth=2, copy=False):
     Yielded arrays are views of pinned buffers that are reused ``depth`` batches later
     unless ``copy=True``.
     """
-    slots, pending = [None] * max(1, int(depth)), deque()
+    # workspaces persist across calls (per host thread): their whole-decode CUDA graphs
+    # are instantiated once
+    cache = getattr(self._local, "stream_slots", None)
+    if cache is None or len(cache) != max(1, int(depth)):
+        cache = self._local.stream_slots = [None] * max(1, int(depth))
+    slots, pending = cache, deque()
 
     def finish(slot):
         slot.state.wait()

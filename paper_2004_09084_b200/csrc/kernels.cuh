@@ -217,7 +217,7 @@ __device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D
 #pragma unroll
         for (int v = 0; v < V; v++) {
             if (j < d) {
-                ph[j][v] = phi_in(fmaxf(fabsf(q[j][v]), eps));
+                ph[j][v] = phi_in(fabsf(q[j][v]));
                 par[v] ^= (q[j][v] < 0.0f);
             } else {
                 ph[j][v] = 0.0f;
@@ -239,13 +239,13 @@ __device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D
             suf += p;
         }
     }
-    const float lo2 = eps * kInvLn2, hi2 = clip * kInvLn2;
+    const float lo2 = eps * kInvLn2;
 #pragma unroll
     for (int j = 0; j < D; j++) {
 #pragma unroll
         for (int v = 0; v < V; v++) {
             if (j < d) {
-                float mag = phi_out(fminf(fmaxf(ph[j][v], lo2), hi2));
+                float mag = phi_out(fmaxf(ph[j][v], lo2));
                 if (clip_r) mag = fminf(mag, clip);
                 const float r = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
                 ph[j][v] = r;
@@ -264,7 +264,7 @@ template <int V>
 __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph)[4][V], const uint32_t (&synbit)[V],
                                                     float eps, float clip, bool clip_r) {
     const float kInvLn2 = 1.4426950408889634f;
-    const float lo2 = eps * kInvLn2, hi2 = clip * kInvLn2;
+    const float lo2 = eps * kInvLn2;
 #pragma unroll
     for (int v = 0; v < V; v++) {
         uint32_t qs[4];
@@ -272,7 +272,7 @@ __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             qs[j] = __float_as_uint(q[j][v]) & 0x80000000u;
-            p[j] = phi_in(fmaxf(fabsf(q[j][v]), eps));
+            p[j] = phi_in(fabsf(q[j][v]));
         }
         const uint32_t par = qs[0] ^ qs[1] ^ qs[2] ^ qs[3] ^ synbit[v];
         const float c = p[0] + p[1], b = p[2] + p[3];
@@ -283,7 +283,7 @@ __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph
         o[3] = c + p[2];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            float mag = phi_out(fminf(fmaxf(o[j], lo2), hi2));
+            float mag = phi_out(fmaxf(o[j], lo2));
             if (clip_r) mag = fminf(mag, clip);
             const float r = __uint_as_float(__float_as_uint(mag) | (qs[j] ^ par));
             ph[j][v] = r;

@@ -73,40 +73,43 @@ __device__ __forceinline__ float phi_fast(float x, float eps, float clip) {
 
 // ---- lean pair used by the FP32 check update (two Phi per edge) -------------------
 //
-// phi_in(x):  ph = Phi(x) / ln2 for x = max(|q|, eps) in natural units.  This value only
-//   enters the messages of the OTHER edges of the check, through Phi(others) whose slope
-//   is ~2 e^-others; an absolute error e in ph therefore moves those messages by at most
-//   ~2 e^-ph * e.  That lets the small-x branch use d = max(1 - t, x - x^2/2) (absolute
-//   error of ph ~1.7e-7 / x, which is multiplied by e^-ph ~ x / 2): every message moves
-//   by < 2e-7 absolute.  Large x keeps the series for relative accuracy, because small
-//   ph values are summed.  Output in log2 units saves the ln2 scaling.  ~15 instructions.
+// Error model.  Outgoing messages r only need ABSOLUTE accuracy: r is added to q to
+// form the posterior and subtracted next sweep, and every tolerance is relative to
+// max(|ref|, 1).  A message error of ~1e-6 absolute is far inside the 1e-4 contract.
+//
+// phi_in(x) = Phi(x) / ln2 for x = |q| (log2 units).  ph_j only reaches the OTHER
+//   edges' messages through Phi(others), whose slope is |Phi'(o)| = 1/sinh(o) <=
+//   1/sinh(ph_j).  With d = 1 - t the absolute error of ph_j is ~1.7e-7 / x (t = e^-x
+//   from MUFU.EX2), and 1/sinh(Phi(x)) ~ x for small x, so every message moves by
+//   < 2e-7: no small-x branch is needed.  d is kept >= 0 (MUFU.EX2 may round e^-tiny
+//   above 1); x = 0 gives ph = inf, which only drives the other messages' magnitudes
+//   to 0 (reference: Phi(23.7 + ...) ~ 1e-10).  Large x (>= 4) uses the series
+//   2t(1 + t^2/3), truncation < 3e-8 relative, because SMALL ph values are summed and
+//   their relative accuracy matters.  12 instructions, 3 MUFU.
 __device__ __forceinline__ float phi_in(float x) {
     const float kNegLog2e = -1.4426950408889634f;
     const float kInvLn2 = 1.4426950408889634f;
     const float t = ex2_approx(x * kNegLog2e);
-    const float d = fmaxf(1.0f - t, fmaf(-0.5f * x, x, x));
+    const float d = fmaxf(1.0f - t, 0.0f);
     const float lg = lg2_approx((1.0f + t) * rcp_approx(d));
-    // x >= 3: Phi = 2t(1 + t^2/3 + t^4/5), t <= 0.05, truncation < 3e-9
-    const float t2 = t * t;
-    const float s = fmaf(t2, fmaf(t2, 2.0f * kInvLn2 / 5.0f, 2.0f * kInvLn2 / 3.0f), 2.0f * kInvLn2);
-    return x >= 3.0f ? t * s : lg;
+    const float s = fmaf(t * t, 2.0f * kInvLn2 / 3.0f, 2.0f * kInvLn2);
+    return x >= 4.0f ? t * s : lg;
 }
 
 // phi_out(y): Phi(x) in natural units for x = y ln2, y = others in log2 units, clamped
-//   to [eps, clip] / ln2 by the caller.  This is the outgoing message magnitude, so it
-//   keeps full accuracy: x < 1/64 uses d = x (1 - x/2 + x^2/6) (truncation < 2e-7),
-//   x < 3 uses d = 1 - t (relative error <= 1.1e-5 at x = 1/64, i.e. <= 2.3e-6 on Phi),
-//   x >= 3 the series.  ~20 instructions.
+//   below at eps / ln2 by the caller (an upper clamp at the clip would change the
+//   result by < Phi(clip) = 1.9e-13 and is omitted).  This is the outgoing magnitude:
+//   x < 1/64 uses d = x (1 - x/2 + x^2/6) (truncation < 2e-7 relative, the large-message
+//   regime), otherwise d = 1 - t (relative error <= 1.1e-5 at x = 1/64, i.e. <= 3e-6 on
+//   Phi there).  For large x the logarithm of a ratio near 1 has ~2e-7 ABSOLUTE error,
+//   which is all a message needs.  14 instructions, 3 MUFU.
 __device__ __forceinline__ float phi_out(float y) {
     const float kLn2 = 0.6931471805599453f;
     const float t = ex2_approx(-y);
     // d = -expm1(-x) with x = y ln2: y (ln2 - ln2^2/2 y + ln2^3/6 y^2)
     const float p = fmaf(y, fmaf(y, 0.0555041086648216f, -0.2402265069591007f), kLn2);
     const float d = y < (1.0f / 64.0f) * 1.4426950408889634f ? y * p : 1.0f - t;
-    const float lg = lg2_approx((2.0f - d) * rcp_approx(d)) * kLn2;
-    const float t2 = t * t;
-    const float s = fmaf(t2, fmaf(t2, 2.0f / 5.0f, 2.0f / 3.0f), 2.0f);
-    return y >= 3.0f * 1.4426950408889634f ? t * s : lg;
+    return lg2_approx((2.0f - d) * rcp_approx(d)) * kLn2;
 }
 
 }  // namespace qcl

@@ -167,13 +167,13 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def read_traffic():
-    """Per-launch DRAM bytes of the layer kernel from the committed ncu summary, if any."""
+def read_traffic(kernel):
+    """Per-launch DRAM bytes of `kernel` (read + write) from the newest committed ncu summary."""
     for p in sorted((ROOT / "profiles").glob("ncu_summary_*.json"), reverse=True):
         try:
             d = json.loads(p.read_text())
-            if d.get("workload") == "configs[2]" and d.get("dram_bytes_per_layer_launch"):
-                return float(d["dram_bytes_per_layer_launch"]), p.name
+            if d.get("workload") == "configs[2]" and d.get("kernel") == kernel and d.get("dram_bytes_per_launch"):
+                return float(d["dram_bytes_per_launch"]), p.name
         except Exception:
             continue
     return None, None
@@ -201,7 +201,7 @@ def run_b200(args):
     dec = q.LayeredDecoder(index, sched, cfg, device=local, precision="fp32")
     plan = dec._plan
     st = _native.State(plan, B, "fp32")
-    st.set_engine(2)  # CUDA events around every sweep, for the roofline
+    st.set_engine(6)  # flow engine with CUDA events around its launch(es), for the roofline
     st.set_llr_synthetic(seed=SEED, snr_idx=0, first_frame=rank * B, snr=SNR)
     st.set_syndrome(None)
     qcfg = dec._qcfg
@@ -269,10 +269,13 @@ def run_b200(args):
     e2e_value = frames * n / e2e_s / 1e6
     peak, peak_kind = peaks()
     per_launch_ms = sweep_ms / max(layer_launches, 1)
-    # algorithmic bytes of all sweeps of the timed steps, spread over the layer launches
+    launches_per_decode = layer_launches / args.steps
+    flow = launches_per_decode == 1
+    kernel = "flow_kernel" if flow else "layer_tma_kernel"
+    # algorithmic bytes of all sweeps of the timed steps, spread over the update-kernel launches
     alg_bytes_launch = BYTES_PER_EDGE_ITER * E * B * ITERS * args.steps / max(layer_launches, 1)
     achieved = alg_bytes_launch / (per_launch_ms / 1e3) / 1e9
-    traffic, traffic_src = read_traffic()
+    traffic, traffic_src = read_traffic(kernel)
     line = {
         "metric": "Mbit/s decoded, rate-0.1 n=10^6 QC-MET-LDPC, SNR 0.161, 50 iters",
         "value": value, "unit": "Mbit/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -292,11 +295,12 @@ def run_b200(args):
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "peak_source": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
-            "kernel": "layer_kernel (one launch per merged layer)",
+            "kernel": ("flow_kernel (one persistent launch per 50-iteration decode, tiles ordered by "
+                       "completion flags)") if flow else "layer_tma_kernel (one launch per merged layer unit)",
             "alg_bytes_per_launch": alg_bytes_launch,
-            "alg_bytes_note": "16 B per expanded edge per iteration x 3,767,500 edges x 64 codewords per sweep, "
-                              "divided by the layer-kernel launches of a sweep",
-            "layer_launches_per_sweep": layer_launches / (ITERS * args.steps),
+            "alg_bytes_note": "16 B per expanded edge per iteration x 3,767,500 edges x 64 codewords x 50 "
+                              "iterations per decode, divided by the update-kernel launches of a decode",
+            "launches_per_decode": launches_per_decode,
             "avg_launch_ms": per_launch_ms,
             "layer_share_of_step": sweep_ms / max(total_ms, 1e-9),
         },

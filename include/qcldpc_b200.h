@@ -120,9 +120,11 @@ int qcl_state_get_llr(qcl_state *st, double *llr);
 /* Device-time breakdown of the last qcl_state_decode: number of layer-kernel launches and
  * their summed CUDA-event time (ms); used by bench.py's roofline. */
 int qcl_state_kernel_stats(qcl_state *st, int64_t *layer_launches, float *layer_ms, int64_t *all_launches);
-/* Select the layer-update engine: 0 = TMA-pipelined kernels (default), 1 = direct
- * register-staged kernels; 2 / 3 = engine 0 / 1 with CUDA events around every sweep
- * (read by qcl_state_kernel_stats). */
+/* Select the layer-update engine: 4 = flow engine (default: one persistent launch per
+ * decode, tiles ordered by completion flags; FP32, row degree <= 12, >= 4 lanes -- other
+ * cases and single-layer calls use engine 0), 0 = TMA-pipelined per-layer kernels,
+ * 1 = direct register-staged kernels; 2 / 3 / 6 = engine 0 / 1 / 4 with CUDA events
+ * around every sweep or flow launch (read by qcl_state_kernel_stats). */
 int qcl_state_set_engine(qcl_state *st, int32_t engine);
 
 /* ---- asynchronous path (streaming / overlapped host<->device copies) ---------------

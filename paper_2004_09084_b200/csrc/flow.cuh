@@ -1,0 +1,447 @@
+// flow.cuh -- persistent dataflow decode (sm_100a): every layer of every iteration in
+// ONE launch, ordered by per-tile completion flags instead of kernel boundaries.
+//
+// Why.  The per-layer engines pay a launch ramp-up and a drain tail at each of the 30
+// layer boundaries of a sweep (1500 per 50-iteration decode): a 2-row layer takes
+// ~10 us although it moves 1.6 us worth of bytes (profiles/r01_launches_2iter_b64.csv).
+// Layered decoding only orders a check after the checks that last wrote ITS variables
+// (decoder.py:259-262 runs layer l+1 on the posteriors written by layer l), and in a
+// QC code those writers are known statically: tile (slot s, checks k0..k0+kt) reads
+// column c at offsets k + shift_s(c); the previous row p touching c wrote the same
+// variables at offsets k + shift_s(c) - shift_p(c) (mod z).  So each tile waits for at
+// most a few tiles of each previous writer, and the next layer starts as soon as the
+// tiles it needs are stored instead of when the whole previous layer has drained.
+//
+// Work items are (iteration t, layer l, lane group g, slot s in l, k-block kb), in that
+// order, claimed with one atomicAdd per tile.  A tile only waits for items claimed
+// before it, so the kernel is deadlock free without co-residency: the smallest unfinished
+// claimed item never waits (its dependencies are smaller, hence finished), and a CTA
+// releases a tile's flag without waiting for anything else.  Lane groups interleave per
+// layer, so with G groups a tile's dependencies were claimed at least (G-1) layer-groups
+// earlier -- normally they are complete before it is claimed.
+//
+// Dependencies (flag[g][slot][kb] = iterations completed by that tile):
+//   * RAW/WAR on posteriors: a tile waits for the previous writer's tiles that cover its
+//     variables of every column (need t+1, or t if the previous writer is the same or a
+//     later slot, i.e. in the previous iteration).  Each edge is a read-modify-write of
+//     its variable by one check, so the RAW wait also orders every earlier read (WAR).
+//   * edge messages R of (s, k) are only touched by (s, k) itself once per iteration;
+//     every path of previous writers from (t-1, s, kb) to (t, s, kb) is a chain of such
+//     waits, so the ordering is transitive (release/acquire at gpu scope).
+//
+// CTA roles (12 warps): warp 0 scheduler (claim, wait for dependencies, queue the tile
+// header), warp 1 loader (bulk-load the tile's 2d runs into a ring stage), warps 2-3
+// storers (alternate ring positions: bulk-store the updated stage, free it, wait for the
+// writes, release the tile flag), warps 4..11 consumers (check update in shared memory,
+// exactly the math of layer_tma_kernel).  The storers are what keep the scheme deadlock
+// free: a scheduler blocked on a dependency never holds a finished tile back, because
+// finished tiles are stored and released by other warps.
+#pragma once
+#include <cstdint>
+
+#include "pipeline.cuh"
+
+namespace qcl {
+
+constexpr int kFlowConsumers = 8;                  // consumer warps per CTA
+constexpr int kFlowStorers = 2;                    // storer warps per CTA
+constexpr int kFlowThreads = 32 * (kFlowConsumers + 2 + kFlowStorers);
+constexpr int kFlowQueue = 4;                      // scheduler -> loader header queue
+constexpr int kFlowStageBytes = 32 * 1024;         // 2*D*KT*W*4 <= 32 KB for every class
+constexpr int kFlowMaxStages = 4;
+constexpr int kFlowHeadBytes = 512;                // mbarriers + stage headers + header queue
+
+// Packed plan tables, copied into shared memory at kernel start (every producer/storer
+// lookup is then an LDS, not a dependent L2 round trip).
+//   slot: x = edge_off | degree << 16 | cls << 24,  y = kb_off (first tile flag in a group)
+//   edge: x = col | reused << 15 | shift << 16,     y = prev_slot | wrap << 15 | delta << 16
+// cls 0: d <= 4 (V 4), 1: d <= 8 (V 2), 2: d <= 12 (V 1); KT = 32 * consumers * V / W.
+// prev_slot/wrap/delta: the previous writer of the column in cyclic schedule order and
+// (shift - prev_shift) mod z; wrap = 1 when that writer runs in the previous iteration.
+struct FlowHdr {  // stage header written by the producer, read by consumers and storers
+    int32_t slot, g, k0, kt, d, cls, t, edge_off;
+};
+
+struct FlowArgs {
+    const uint2 *slot_tab;   // [S]
+    const uint2 *edge_tab;   // [E]
+    const int2 *items;       // per item of one sweep: {slot | g << 16, kb}
+    int32_t sweep_items;     // items per sweep
+    int32_t item_begin, item_end;  // global item range of this launch (t * sweep_items + ...)
+    int *counter;            // claim counter of this launch (zeroed before it)
+    int *flags;              // [G][nkb_total] iterations completed per tile
+    int32_t nkb_total;
+    void *L, *R;
+    const uint8_t *syn;
+    int64_t n;
+    int32_t E, S, z, lw;
+    int32_t stages;
+    int32_t clip_r;
+    const int *n_active;  // early termination: skip the launch once every frame converged
+    unsigned long long *stats;  // optional instrumentation (QCL_FLOW_STATS)
+    double clip, eps;
+};
+
+__host__ __device__ constexpr int flow_class_V(int cls) { return cls == 0 ? 4 : cls == 1 ? 2 : 1; }
+__host__ __device__ constexpr int flow_class_D(int cls) { return cls == 0 ? 4 : cls == 1 ? 8 : 12; }
+__host__ __device__ constexpr size_t flow_smem_bytes(int S, int E, int stages) {
+    return ((kFlowHeadBytes + 8 * (size_t)(S + E) + 127) / 128) * 128 + (size_t)stages * kFlowStageBytes;
+}
+
+__device__ __forceinline__ int ld_relaxed(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int *p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Poll a tile flag.  Relaxed loads go to L2 (the point of coherence the storer released
+// the flag to, after its bulk writes completed); the bulk copies issued after the poll
+// loop exits are control dependent on the observed value and also read L2, and the
+// fence.proxy.async that follows orders them after the poll.  No gpu-scope acquire
+// fence: it would cost a MEMBAR.ALL.GPU plus an L1 invalidation per tile.
+__device__ __forceinline__ int spin_until(const int *flag, int need) {
+    if (ld_relaxed(flag) >= need) return 0;
+    int polls = 1;
+    while (ld_relaxed(flag) < need) {
+        __nanosleep(64);
+        polls++;
+    }
+    return polls;
+}
+
+// Bulk runs of one tile (LOAD: global -> stage, else stage -> global); lane j: edge j.
+__device__ __forceinline__ void flow_runs(const FlowArgs &a, const FlowHdr &h, const uint2 *etab, int KT, int D,
+                                          float *stage, uint64_t *bar, bool load, uint64_t pol_keep,
+                                          uint64_t pol_stream) {
+    const int lane = threadIdx.x & 31;
+    const int W = 1 << a.lw, z = a.z;
+    const int KTW = KT * W;
+    float *Lg = reinterpret_cast<float *>(a.L) + (((size_t)h.g * a.n) << a.lw);
+    float *Rg = reinterpret_cast<float *>(a.R) + ((((size_t)h.g * a.E + h.edge_off) * z + h.k0) << a.lw);
+    for (int j = lane; j < h.d; j += 32) {
+        const uint32_t ex = etab[h.edge_off + j].x;
+        const int col = ex & 0x7fff, shift = ex >> 16;
+        const bool reused = (ex >> 15) & 1;
+        int p0 = h.k0 + shift;
+        p0 -= (p0 >= z) ? z : 0;
+        const int len1 = min(h.kt, z - p0);
+        const uint32_t b1 = (uint32_t)len1 * W * 4;
+        const uint32_t b2 = (uint32_t)(h.kt - len1) * W * 4;
+        const uint32_t br = (uint32_t)h.kt * W * 4;
+        const uint64_t pl = reused ? pol_keep : pol_stream;
+        const size_t vb = (size_t)col * z;
+        float *lg1 = Lg + ((vb + p0) << a.lw);
+        float *lg2 = Lg + (vb << a.lw);
+        float *rg = Rg + ((size_t)j * z << a.lw);
+        float *ls = stage + (size_t)j * KTW;
+        float *rs = stage + (size_t)(D + j) * KTW;
+        if (load) {
+            bulk_load(ls, lg1, b1, bar, pl);
+            if (b2) bulk_load(ls + (size_t)len1 * W, lg2, b2, bar, pl);
+            bulk_load(rs, rg, br, bar, pol_stream);
+        } else {
+            bulk_store(lg1, ls, b1, pl);
+            if (b2) bulk_store(lg2, ls + (size_t)len1 * W, b2, pl);
+            bulk_store(rg, rs, br, pol_stream);
+        }
+    }
+}
+
+// One consumer thread: check (ci) of the tile for V lanes, in place in the stage.
+template <int V, int D, bool HAS_SYN>
+__device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
+                                             const LayerArgs &la) {
+    const int W = 1 << a.lw;
+    const int KT = kFlowConsumers * 32 * V / W;
+    const int KTW = KT * W;
+    const int lanes_v = W / V;
+    const int ci = ct / lanes_v;
+    const int w0 = (ct - ci * lanes_v) * V;
+    if (ci >= h.kt) return;
+    const int off = ci * W + w0;
+    const float clip = (float)a.clip;
+    using VT = typename Vec<float, V>::type;
+    float q[D][V], ph[D][V];
+    int par[V];
+    if (HAS_SYN) {
+        const uint8_t *sp = a.syn + ((((int64_t)h.g * a.S + h.slot) * a.z + h.k0 + ci) << a.lw) + w0;
+#pragma unroll
+        for (int v = 0; v < V; v++) par[v] = sp[v] & 1;
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; v++) par[v] = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+        if (j < h.d) {
+            float lv[V], rv[V];
+            *reinterpret_cast<VT *>(lv) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
+            *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+#pragma unroll
+            for (int v = 0; v < V; v++) q[j][v] = clampT(lv[v] - rv[v], clip);
+        } else {
+#pragma unroll
+            for (int v = 0; v < V; v++) q[j][v] = 0.0f;
+        }
+    }
+    check_update<V, D>(q, ph, par, h.d, la);
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+        if (j < h.d) {
+            *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(ph[j]);
+            *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(q[j]);
+        }
+    }
+}
+
+#define FLOW_TICK(k)                          \
+    if (prof) {                               \
+        const long long c_ = clock64();       \
+        acc[k] += c_ - tc;                    \
+        tc = c_;                              \
+    }
+
+template <bool HAS_SYN>
+__global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
+    if (a.n_active && *(volatile const int *)a.n_active == 0) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);  // loader -> consumers (+tx)
+    uint64_t *done = full + kFlowMaxStages;                    // consumers -> storers
+    uint64_t *empty = done + kFlowMaxStages;                   // storers -> loader
+    uint64_t *ready = empty + kFlowMaxStages;                  // scheduler -> loader (queue)
+    uint64_t *qfree = ready + kFlowQueue;                      // loader -> scheduler (queue)
+    FlowHdr *hdr = reinterpret_cast<FlowHdr *>(smem_raw + 256);
+    FlowHdr *hq = hdr + kFlowMaxStages;
+    uint2 *stab = reinterpret_cast<uint2 *>(smem_raw + kFlowHeadBytes);
+    uint2 *etab = stab + a.S;
+    float *stages = reinterpret_cast<float *>(smem_raw + ((kFlowHeadBytes + 8 * (size_t)(a.S + a.E) + 127) / 128) * 128);
+    constexpr size_t kStageElems = kFlowStageBytes / 4;
+    const int S = a.stages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int W = 1 << a.lw;
+
+    for (int i = threadIdx.x; i < a.S; i += blockDim.x) stab[i] = a.slot_tab[i];
+    for (int i = threadIdx.x; i < a.E; i += blockDim.x) etab[i] = a.edge_tab[i];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&done[s], kFlowConsumers);
+            mbar_init(&empty[s], 1);
+        }
+        for (int q = 0; q < kFlowQueue; q++) {
+            mbar_init(&ready[q], 1);
+            mbar_init(&qfree[q], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const bool prof = a.stats != nullptr;
+    long long acc[4] = {0, 0, 0, 0}, tc = 0;
+
+    if (warp == 0) {
+        // ----------------------------------------------------------------- scheduler
+        // claims run two items ahead and the item record one ahead, so neither L2 round
+        // trip is on the tile's critical path.  Holding claimed items is deadlock free:
+        // they are larger than the item in hand.  Resolved headers go to the loader warp
+        // through a small queue, so dependency polling overlaps the bulk-copy issue.
+        int n2 = 0;
+        if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
+        int n1 = __shfl_sync(0xffffffffu, n2, 0);
+        int2 r1 = make_int2(0, 0);
+        if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
+        if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
+        int sentinels = 0;
+        for (int it = 0, q = 0, ph = 0;; it++) {
+            if (prof) tc = clock64();
+            if (it >= kFlowQueue) mbar_wait(&qfree[q], ph ^ 1);
+            FLOW_TICK(0);
+            const int item = n1;
+            const int2 e = r1;
+            if (item >= a.item_end) {
+                // one end marker per storer warp, at consecutive ring positions
+                if (lane == 0) {
+                    hq[q].kt = -1;
+                    mbar_arrive(&ready[q]);
+                }
+                if (++sentinels == kFlowStorers) break;
+            } else {
+                n1 = __shfl_sync(0xffffffffu, n2, 0);
+                if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
+                if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
+                FLOW_TICK(1);
+                FlowHdr h;
+                h.t = item / a.sweep_items;
+                h.slot = e.x & 0xffff;
+                h.g = e.x >> 16;
+                const uint2 st = stab[h.slot];
+                h.edge_off = st.x & 0xffff;
+                h.d = (st.x >> 16) & 0xff;
+                h.cls = st.x >> 24;
+                const int KT = kFlowConsumers * 32 * flow_class_V(h.cls) / W;
+                h.k0 = e.y * KT;
+                h.kt = min(KT, a.z - h.k0);
+                // wait for the previous writers of every column of this tile
+                int polls = 0;
+                const int *fg = a.flags + (size_t)h.g * a.nkb_total;
+                for (int j = lane; j < h.d; j += 32) {
+                    const uint32_t dy = etab[h.edge_off + j].y;
+                    const int need = h.t + 1 - (int)((dy >> 15) & 1);
+                    if (need <= 0) continue;
+                    const uint2 pst = stab[dy & 0x7fff];
+                    const int KTp = kFlowConsumers * 32 * flow_class_V(pst.x >> 24) / W;
+                    const int *fl = fg + pst.y;
+                    int a0 = h.k0 + (int)(dy >> 16);
+                    a0 -= (a0 >= a.z) ? a.z : 0;
+                    const int b = a0 + h.kt - 1;
+                    const int hi = min(b, a.z - 1);
+                    for (int kb = a0 / KTp; kb <= hi / KTp; kb++) polls += spin_until(fl + kb, need);
+                    if (b >= a.z)
+                        for (int kb = 0; kb <= (b - a.z) / KTp; kb++) polls += spin_until(fl + kb, need);
+                }
+                FLOW_TICK(2);
+                if (prof) {
+                    polls = __reduce_add_sync(0xffffffffu, polls);
+                    if (lane == 0) {
+                        if (polls) atomicAdd(a.stats, 1ull);
+                        atomicAdd(a.stats + 1, (unsigned long long)polls);
+                        atomicAdd(a.stats + 2, 1ull);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    hq[q] = h;
+                    mbar_arrive(&ready[q]);  // release: the loader's bulk reads follow these polls
+                }
+                FLOW_TICK(3);
+            }
+            if (++q == kFlowQueue) {
+                q = 0;
+                ph ^= 1;
+            }
+        }
+        if (prof && lane == 0)
+            for (int k = 0; k < 4; k++) atomicAdd(a.stats + 3 + k, (unsigned long long)acc[k]);
+        return;
+    }
+
+    if (warp == 1) {
+        // -------------------------------------------------------------------- loader
+        const uint64_t pol_stream = policy_evict_first();
+        const uint64_t pol_keep = policy_evict_last();
+        int sentinels = 0;
+        for (int it = 0, s = 0, ph = 0, q = 0, qph = 0;; it++) {
+            mbar_wait(&ready[q], qph);
+            const FlowHdr h = hq[q];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&qfree[q]);
+            if (++q == kFlowQueue) {
+                q = 0;
+                qph ^= 1;
+            }
+            if (it >= S) mbar_wait(&empty[s], ph ^ 1);
+            if (h.kt < 0) {
+                if (lane == 0) {
+                    hdr[s].kt = -1;
+                    mbar_arrive(&full[s]);
+                }
+                if (++sentinels == kFlowStorers) break;
+            } else {
+                fence_proxy_async_global();  // observed flags -> ordered before the bulk (async proxy) reads
+                const int KT = kFlowConsumers * 32 * flow_class_V(h.cls) / W;
+                if (lane == 0) {
+                    hdr[s] = h;
+                    mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * h.d * h.kt * W * 4));
+                }
+                __syncwarp();
+                flow_runs(a, h, etab, KT, flow_class_D(h.cls), stages + (size_t)s * kStageElems, &full[s], true,
+                          pol_keep, pol_stream);
+            }
+            if (++s == S) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+        return;
+    }
+
+    if (warp <= 1 + kFlowStorers) {
+        // ------------------------------------------------------------------- storers
+        // storer k takes ring positions k, k + kFlowStorers, ...: one warp's wait for its
+        // writes to complete overlaps the other's stores
+        const uint64_t pol_stream = policy_evict_first();
+        const uint64_t pol_keep = policy_evict_last();
+        const bool sprof = prof && warp == 2;
+        for (int it = warp - 2;; it += kFlowStorers) {
+            const int s = it % S;
+            if (sprof) tc = clock64();
+            mbar_wait(&done[s], (it / S) & 1);
+            if (sprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
+            const FlowHdr h = hdr[s];
+            if (h.kt < 0) break;
+            const int KT = kFlowConsumers * 32 * flow_class_V(h.cls) / W;
+            flow_runs(a, h, etab, KT, flow_class_D(h.cls), stages + (size_t)s * kStageElems, nullptr, false,
+                      pol_keep, pol_stream);
+            bulk_commit();
+            if (sprof) { const long long c_ = clock64(); acc[1] += c_ - tc; tc = c_; }
+            bulk_wait_read_all();  // the stage may be refilled once its bytes are read out
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (sprof) { const long long c_ = clock64(); acc[2] += c_ - tc; tc = c_; }
+            bulk_wait_all();  // this lane's writes are performed ...
+            fence_proxy_async_global();
+            __syncwarp();
+            if (lane == 0)  // ... before the tile is released to its dependents
+                st_release(a.flags + (size_t)h.g * a.nkb_total + stab[h.slot].y + h.k0 / KT, h.t + 1);
+            if (sprof) acc[3] += clock64() - tc;
+        }
+        if (sprof && lane == 0)
+            for (int k = 0; k < 4; k++) atomicAdd(a.stats + 9 + k, (unsigned long long)acc[k]);
+        return;
+    }
+
+    // ---------------------------------------------------------------------- consumers
+    const int ct = threadIdx.x - 32 * (2 + kFlowStorers);
+    const bool cprof = prof && warp == 2 + kFlowStorers;
+    LayerArgs la;
+    la.uniform = 0;
+    la.clip_r = a.clip_r;
+    la.clip = a.clip;
+    la.eps = a.eps;
+    int sentinels = 0;
+    for (int s = 0, ph = 0;;) {
+        if (cprof) tc = clock64();
+        mbar_wait(&full[s], ph);
+        if (cprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
+        const FlowHdr h = hdr[s];
+        if (h.kt < 0) {
+            if (lane == 0) mbar_arrive(&done[s]);
+            if (++sentinels == kFlowStorers) break;
+        } else {
+            float *stage = stages + (size_t)s * kStageElems;
+            if (h.cls == 0)
+                flow_consume<4, 4, HAS_SYN>(a, h, stage, ct, la);
+            else if (h.cls == 1)
+                flow_consume<2, 8, HAS_SYN>(a, h, stage, ct, la);
+            else
+                flow_consume<1, 12, HAS_SYN>(a, h, stage, ct, la);
+            fence_proxy_async_smem();  // this thread's STS -> visible to the bulk-store engine
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&done[s]);
+            if (cprof) acc[1] += clock64() - tc;
+        }
+        if (++s == S) {
+            s = 0;
+            ph ^= 1;
+        }
+    }
+    if (cprof && lane == 0)
+        for (int k = 0; k < 2; k++) atomicAdd(a.stats + 7 + k, (unsigned long long)acc[k]);
+}
+#undef FLOW_TICK
+
+}  // namespace qcl

@@ -21,6 +21,7 @@
 #include "../../include/qcldpc_b200.h"
 #include "kernels.cuh"
 #include "pipeline.cuh"
+#include "flow.cuh"
 
 using namespace qcl;
 
@@ -65,6 +66,9 @@ struct qcl_plan {
     std::vector<SlotInfo> h_slots;
     SlotInfo *slots = nullptr;  // device H_compact1: per slot
     EdgeInfo *edges = nullptr;  // device H_compact1: per circulant
+    uint2 *fedge_tab = nullptr;  // device, flow engine: packed circulant + previous-writer table
+    bool flow_ok = false;        // the code fits the flow engine's packed tables
+    std::vector<int32_t> h_edge_shift, h_edge_col;
     std::mutex cache_mu;
     std::vector<qcl_state *> cache;  // idle states reused by qcl_decode
 };
@@ -94,7 +98,7 @@ struct qcl_state {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_done = nullptr;
     void *staging2 = nullptr;  // syndrome staging (async path: LLR staging may still be in flight)
     size_t staging2_bytes = 0;
-    int engine = 0;
+    int engine = 4;  // flow engine where eligible, else the TMA per-layer kernels
     // per-sweep CUDA graph, rebuilt when clip/eps/syndrome presence change
     cudaGraphExec_t sweep_exec = nullptr;
     double g_clip = -1, g_eps = -1;
@@ -110,6 +114,14 @@ struct qcl_state {
     int64_t launches_layer = 0, launches_all = 0, sweep_launches = 0;
     bool profiling = false;
     float layer_ms = 0;
+    // flow engine (engine 4): tiling, item list, tile flags and claim counters
+    uint2 *fslot_tab = nullptr;
+    int2 *fitems = nullptr;
+    int *fflags = nullptr, *fcounters = nullptr;
+    unsigned long long *fstats = nullptr;  // QCL_FLOW_STATS=1: dependency-wait counters
+    int64_t f_sweep_items = 0;
+    int32_t f_nkb_total = 0, f_counter_cap = 0, f_grid = 0, f_stages = 3;
+    bool flow_decode = false;  // this decode runs on the flow engine
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sweep_events;
 };
 
@@ -242,8 +254,9 @@ static void launch_tma(const PipeArgs &a, int V, int dmax, cudaStream_t stream, 
 static int dmax_bucket(int d) { return d <= 4 ? 4 : d <= 8 ? 8 : d <= 12 ? 12 : d <= 16 ? 16 : 32; }
 
 static bool use_tma(const qcl_state *st) {
-    // bulk copies move whole lane rows: W * sizeof(T) must be a 16-byte multiple
-    return st->engine == 0 && ((size_t)st->W * st->esz) % 16 == 0;
+    // bulk copies move whole lane rows: W * sizeof(T) must be a 16-byte multiple; the flow
+    // engine (4) uses these kernels for single layers and for codes/precisions it does not cover
+    return (st->engine == 0 || st->engine == 4) && ((size_t)st->W * st->esz) % 16 == 0;
 }
 
 static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t stream, double clip, double eps,
@@ -374,6 +387,123 @@ static void enqueue_sweep(qcl_state *st, double clip, double eps) {
         cudaEventRecord(st->join[c - 1], st->side[c - 1]);
         cudaStreamWaitEvent(st->stream, st->join[c - 1], 0);
     }
+}
+
+// ------------------------------------------------------------ flow engine (engine 4)
+// One persistent launch runs many sweeps; tiles are ordered by completion flags
+// (csrc/flow.cuh).  FP32 only, row degree <= 12, and W >= 4 lanes (16-byte bulk runs).
+static bool use_flow(const qcl_state *st) {
+    return st->engine == 4 && st->prec == QCL_PREC_FP32 && st->plan->flow_ok && st->plan->max_degree <= 12 &&
+           st->W >= 4 && st->f_grid >= 0;
+}
+
+// Tiling (per slot), the item list of one sweep and the flag/counter buffers.
+static int ensure_flow(qcl_state *st, int counters) {
+    const qcl_plan *p = st->plan;
+    if (!st->fslot_tab) {
+        std::vector<uint2> stab(p->S);
+        std::vector<int> nkb(p->S);
+        int32_t off = 0;
+        for (int s = 0; s < p->S; s++) {
+            const int d = p->h_slots[s].degree;
+            const uint32_t cls = d <= 4 ? 0 : d <= 8 ? 1 : 2;
+            const int KT = kFlowConsumers * 32 * flow_class_V(cls) / st->W;
+            nkb[s] = (int)cdiv(p->z, KT);
+            stab[s].x = (uint32_t)p->h_slots[s].edge_off | ((uint32_t)d << 16) | (cls << 24);
+            stab[s].y = (uint32_t)off;
+            off += nkb[s];
+        }
+        st->f_nkb_total = off;
+        // item order: iteration, layer, lane group, slot, k-block (flow.cuh)
+        std::vector<int2> items;
+        for (int l = 0; l < p->n_layers; l++)
+            for (int g = 0; g < st->G; g++)
+                for (int s = p->layer_start[l]; s < p->layer_start[l + 1]; s++)
+                    for (int kb = 0; kb < nkb[s]; kb++) items.push_back(make_int2(s | (g << 16), kb));
+        st->f_sweep_items = (int64_t)items.size();
+        CK(cudaMalloc(&st->fslot_tab, sizeof(uint2) * p->S));
+        CK(cudaMemcpy(st->fslot_tab, stab.data(), sizeof(uint2) * p->S, cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&st->fitems, sizeof(int2) * items.size()));
+        CK(cudaMemcpy(st->fitems, items.data(), sizeof(int2) * items.size(), cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&st->fflags, sizeof(int) * (size_t)st->G * st->f_nkb_total));
+        if (env_int("QCL_FLOW_STATS", 0)) {
+            CK(cudaMalloc(&st->fstats, 16 * sizeof(unsigned long long)));
+            CK(cudaMemset(st->fstats, 0, 16 * sizeof(unsigned long long)));
+        }
+        // ring depth: QCL_FLOW_STAGES (default 3), reduced until two CTAs fit per SM
+        static int want = env_int("QCL_FLOW_STAGES", 3);
+        int stages = std::max(2, std::min(want, kFlowMaxStages));
+        int sms = 0, per_sm = 0, max_smem = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
+        CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device));
+        while (stages > 2 && flow_smem_bytes(p->S, p->E, stages) * 2 + 2048 > 233472) stages--;
+        const size_t smem = flow_smem_bytes(p->S, p->E, stages);
+        if ((int64_t)smem > max_smem) {
+            st->f_grid = -1;  // tables too large: the per-layer engine runs instead
+            return QCL_OK;
+        }
+        st->f_stages = stages;
+        for (auto kern : {flow_kernel<false>, flow_kernel<true>})
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<false>, kFlowThreads, smem));
+        st->f_grid = sms * std::max(1, per_sm);
+    }
+    if (st->f_counter_cap < counters) {
+        if (st->fcounters) cudaFree(st->fcounters);
+        st->fcounters = nullptr;
+        st->f_counter_cap = 0;
+        CK(cudaMalloc(&st->fcounters, sizeof(int) * counters));
+        st->f_counter_cap = counters;
+    }
+    return QCL_OK;
+}
+
+// Flags and claim counters back to zero: the start of a flow decode (sweep 0).
+static int enqueue_flow_reset(qcl_state *st, int counters) {
+    int rc = ensure_flow(st, counters);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(st->fflags, 0, sizeof(int) * (size_t)st->G * st->f_nkb_total, st->stream));
+    CK(cudaMemsetAsync(st->fcounters, 0, sizeof(int) * counters, st->stream));
+    return QCL_OK;
+}
+
+// Sweeps [t0, t0 + T) in one persistent launch using claim counter `counter`.
+static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, int counter, bool et) {
+    const qcl_plan *p = st->plan;
+    FlowArgs a;
+    a.slot_tab = st->fslot_tab;
+    a.edge_tab = p->fedge_tab;
+    a.items = st->fitems;
+    a.sweep_items = (int32_t)st->f_sweep_items;
+    a.item_begin = (int32_t)(t0 * st->f_sweep_items);
+    a.item_end = (int32_t)((t0 + T) * st->f_sweep_items);
+    a.counter = st->fcounters + counter;
+    a.flags = st->fflags;
+    a.nkb_total = st->f_nkb_total;
+    a.L = st->L;
+    a.R = st->R;
+    a.syn = st->has_syn ? st->syn : nullptr;
+    a.n = p->n;
+    a.E = p->E;
+    a.S = p->S;
+    a.z = p->z;
+    a.lw = st->lw;
+    a.stages = st->f_stages;
+    a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));  // |r| <= Phi(eps)
+    a.n_active = et ? st->n_active : nullptr;
+    a.stats = st->fstats;
+    a.clip = clip;
+    a.eps = eps;
+    const size_t smem = flow_smem_bytes(p->S, p->E, st->f_stages);
+    const int64_t grid = std::min<int64_t>(st->f_grid, a.item_end - a.item_begin);
+    if (st->has_syn)
+        flow_kernel<true><<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
+    else
+        flow_kernel<false><<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
+    CK(cudaGetLastError());
+    st->launches_layer++;
+    st->launches_all++;
+    return QCL_OK;
 }
 
 // Hard decisions of every lane packed into sign words (decoder.py:264-266).
@@ -578,7 +708,33 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
         p->layer_unit0.push_back((int)p->units.size());
         p->h_slot_list = list;
     }
+    // flow engine: per circulant the previous writer of its column in cyclic schedule
+    // (= slot) order; the first toucher of a column waits on the last one of the previous
+    // iteration (itself for a degree-1 column).  Packed as in csrc/flow.cuh.
+    std::vector<uint2> h_etab(n_edges);
+    p->flow_ok = z <= 65535 && n_cols <= 32767 && n_slots <= 32767 && n_edges <= 65535;
+    {
+        std::vector<std::vector<int>> touch(n_cols);  // circulants per column, slot order
+        for (int e = 0; e < n_edges; e++) touch[edge_col[e]].push_back(e);
+        std::vector<int> slot_of(n_edges);
+        for (int s = 0; s < n_slots; s++)
+            for (int e = slot_offsets[s]; e < slot_offsets[s + 1]; e++) slot_of[e] = s;
+        for (int c = 0; c < n_cols; c++) {
+            const auto &tl = touch[c];
+            for (size_t i = 0; i < tl.size(); i++) {
+                const int e = tl[i], pe = i ? tl[i - 1] : tl.back();
+                int delta = edge_shift[e] - edge_shift[pe];
+                delta += delta < 0 ? z : 0;
+                const uint32_t reused = tl.size() > 1;
+                h_etab[e].x = (uint32_t)(c & 0x7fff) | (reused << 15) | ((uint32_t)edge_shift[e] << 16);
+                h_etab[e].y = (uint32_t)(slot_of[pe] & 0x7fff) | ((i == 0 ? 1u : 0u) << 15) | ((uint32_t)delta << 16);
+            }
+        }
+    }
     cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaMalloc(&p->fedge_tab, sizeof(uint2) * n_edges);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->fedge_tab, h_etab.data(), sizeof(uint2) * n_edges, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&p->slot_list, sizeof(int32_t) * p->h_slot_list.size());
     if (e == cudaSuccess)
         e = cudaMemcpy(p->slot_list, p->h_slot_list.data(), sizeof(int32_t) * p->h_slot_list.size(),
@@ -593,6 +749,7 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
         cudaFree(p->slots);
         cudaFree(p->edges);
         cudaFree(p->slot_list);
+        cudaFree(p->fedge_tab);
         delete p;
         return fail(QCL_ECUDA, "plan upload failed: %s", cudaGetErrorString(e));
     }
@@ -609,6 +766,7 @@ int qcl_plan_destroy(qcl_plan *p) {
     cudaFree(p->slots);
     cudaFree(p->edges);
     cudaFree(p->slot_list);
+    cudaFree(p->fedge_tab);
     delete p;
     return QCL_OK;
 }
@@ -691,12 +849,25 @@ int qcl_state_destroy(qcl_state *st) {
     if (!st) return QCL_OK;
     cudaSetDevice(st->plan->device);
     if (st->stream) cudaStreamSynchronize(st->stream);
+    if (st->fstats) {
+        unsigned long long h[16] = {};
+        cudaMemcpy(h, st->fstats, sizeof(h), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[flow stats] B=%lld W=%d tiles=%llu waited=%llu (%.2f%%) polls=%llu\n", (long long)st->B,
+                st->W, h[2], h[0], h[2] ? 100.0 * h[0] / h[2] : 0.0, h[1]);
+        const double T = h[2] ? (double)h[2] : 1.0;
+        fprintf(stderr, "[flow stats] cycles/tile scheduler: qfree %.0f claim %.0f deps %.0f queue %.0f | "
+                        "consumer: full-wait %.0f compute %.0f | storer(x2 tiles): done-wait %.0f issue %.0f "
+                        "read %.0f write+release %.0f\n",
+                h[3] / T, h[4] / T, h[5] / T, h[6] / T, h[7] / T, h[8] / T, 2 * h[9] / T, 2 * h[10] / T,
+                2 * h[11] / T, 2 * h[12] / T);
+    }
     if (st->sweep_exec) cudaGraphExecDestroy(st->sweep_exec);
     if (st->decode_exec) cudaGraphExecDestroy(st->decode_exec);
     for (void *ptr : {st->llr, st->L, st->R, (void *)st->syn, (void *)st->words, (void *)st->conv,
                       (void *)st->unsat, (void *)st->signs, (void *)st->synpack, (void *)st->active,
                       (void *)st->take, (void *)st->iters,
-                      (void *)st->n_active, (void *)st->truths, st->staging})
+                      (void *)st->n_active, (void *)st->truths, st->staging, (void *)st->fslot_tab,
+                      (void *)st->fitems, (void *)st->fflags, (void *)st->fcounters, (void *)st->fstats})
         if (ptr) cudaFree(ptr);
     if (st->h_n_active) cudaFreeHost(st->h_n_active);
     if (st->h_flag) cudaFreeHost(st->h_flag);
@@ -938,6 +1109,21 @@ int qcl_state_layers(qcl_state *st, int32_t first, int32_t count, double llr_cli
     CK(cudaSetDevice(p->device));
     const bool saved_et = st->g_et;
     st->g_et = false;  // direct layer launches never skip
+    if (use_flow(st) && first == 0 && count == p->n_layers) {
+        int rc = ensure_flow(st, 1);
+        if (rc) {
+            st->g_et = saved_et;
+            return rc;
+        }
+    }
+    if (use_flow(st) && first == 0 && count == p->n_layers) {  // one whole sweep: flow engine
+        int rc = enqueue_flow_reset(st, 1);
+        if (!rc) rc = enqueue_flow(st, llr_clip, phi_epsilon, 0, 1, 0, false);
+        st->g_et = saved_et;
+        if (rc) return rc;
+        CK(cudaStreamSynchronize(st->stream));
+        return QCL_OK;
+    }
     for (int l = first; l < first + count; l++) enqueue_layer(st, l, llr_clip, phi_epsilon, st->stream, 0, st->G, true);
     st->g_et = saved_et;
     CK(cudaGetLastError());
@@ -994,9 +1180,23 @@ static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
     st->launches_all++;
     if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
     st->g_et = et;
+    const bool flow = st->flow_decode;
+    if (flow) {
+        if ((rc = enqueue_flow_reset(st, et ? cfg->max_iterations : 1))) return rc;
+        if (!et) {  // every sweep in one persistent launch
+            if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, 0, cfg->max_iterations, 0, false)))
+                return rc;
+        }
+    }
     for (int t = 1; t <= cfg->max_iterations; t++) {
+        if (flow && !et) break;
         const int64_t before = st->launches_layer;
-        enqueue_sweep(st, cfg->llr_clip, cfg->phi_epsilon);
+        if (flow) {
+            if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, t - 1, 1, t - 1, true))) return rc;
+            st->launches_all -= st->launches_layer - before;  // counted below
+        } else {
+            enqueue_sweep(st, cfg->llr_clip, cfg->phi_epsilon);
+        }
         st->launches_all += st->launches_layer - before;
         if (!et) continue;
         if ((rc = enqueue_check(st))) return rc;
@@ -1028,6 +1228,8 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     st->launches_layer = st->launches_all = 0;
     st->layer_ms = 0;
     const bool et = cfg->early_termination != 0;
+    if (use_flow(st) && (rc = ensure_flow(st, cfg->max_iterations))) return rc;  // allocations outside capture
+    st->flow_decode = use_flow(st) && (int64_t)cfg->max_iterations * st->f_sweep_items + 8LL * st->f_grid < (1LL << 31);
     if (!st->profiling && !(sync && et)) {
         const bool stale = !st->decode_exec || st->d_clip != cfg->llr_clip || st->d_eps != cfg->phi_epsilon ||
                            st->d_syn != st->has_syn || st->d_et != et || st->d_iters != cfg->max_iterations ||
@@ -1067,8 +1269,27 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     st->launches_all++;
     if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
     const unsigned gb = (unsigned)cdiv(st->B, kBlock);
+    const bool flow = st->flow_decode;
+    if (flow && (rc = enqueue_flow_reset(st, cfg->max_iterations))) return rc;
     for (int t = 1; t <= cfg->max_iterations; t++) {
-        if ((rc = run_sweep(st, cfg->llr_clip, cfg->phi_epsilon, et))) return rc;
+        if (flow) {
+            // no early termination: all sweeps in one launch (timed as one "sweep" unit)
+            const int T = et ? 1 : cfg->max_iterations;
+            cudaEvent_t a = nullptr, b = nullptr;
+            if (st->profiling) {
+                CK(cudaEventCreate(&a));
+                CK(cudaEventCreate(&b));
+                CK(cudaEventRecord(a, st->stream));
+            }
+            if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, t - 1, T, t - 1, et))) return rc;
+            if (st->profiling) {
+                CK(cudaEventRecord(b, st->stream));
+                st->sweep_events.push_back({a, b});
+            }
+            if (!et) break;
+        } else if ((rc = run_sweep(st, cfg->llr_clip, cfg->phi_epsilon, et))) {
+            return rc;
+        }
         if (!et) continue;
         if ((rc = enqueue_check(st))) return rc;
         et_update_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, t, st->unsat, st->lw, st->active, st->take, st->conv,
@@ -1191,6 +1412,11 @@ int qcl_state_kernel_stats(qcl_state *st, int64_t *layer_launches, float *layer_
 
 int qcl_state_set_engine(qcl_state *st, int32_t engine) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
+    if (engine == 4 || engine == 6) {  // flow engine (persistent dataflow decode); 6: with CUDA events
+        st->profiling = engine == 6;
+        st->engine = 4;
+        return QCL_OK;
+    }
     if (engine == 2 || engine == 3) {  // engine 0/1 plus CUDA events around every sweep (bench roofline)
         st->profiling = true;
         st->engine = engine - 2;

@@ -122,7 +122,7 @@ class LayeredDecoder:
     instance can be shared by a ThreadPoolExecutor like the reference's.
     """
 
-    def __init__(self, index, schedule, cfg, device=0, precision="fp32", engine=0):
+    def __init__(self, index, schedule, cfg, device=0, precision="fp32", engine=4):
         flat_rows = tuple(r for layer in schedule.layers for r in layer)
         if flat_rows != tuple(index.slot_rows):
             raise ValueError("schedule does not match the compact index row order")
@@ -132,7 +132,7 @@ class LayeredDecoder:
         self.index = index
         self.schedule = schedule
         self.precision = precision
-        self.engine = int(engine)  # 0: TMA-pipelined layer kernels, 1: direct kernels
+        self.engine = int(engine)  # 4: flow engine (default), 0: TMA per-layer kernels, 1: direct kernels
         self.device = int(device)
         self.z = int(index.z)
         self.n_vars = int(index.n_cols) * self.z

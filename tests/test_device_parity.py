@@ -84,7 +84,7 @@ def golden_code(name):
     return load_code("standin_v2_z100")
 
 
-@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("engine", [0, 1, 4])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 @pytest.mark.parametrize("name", LAYER_CASES)
 def test_layer_and_sweeps_match_reference(gpu, name, precision, engine):
@@ -121,7 +121,7 @@ def test_layer_and_sweeps_match_reference(gpu, name, precision, engine):
 
 
 @pytest.mark.parametrize("batch", [2, 4, 8])
-@pytest.mark.parametrize("engine", [0, 1])
+@pytest.mark.parametrize("engine", [0, 1, 4])
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 def test_layer_from_reference_state_with_messages(gpu, precision, engine, batch):
     """One layer from a mid-decode reference state (nonzero messages), per layer.

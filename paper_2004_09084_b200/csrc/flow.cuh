@@ -80,6 +80,7 @@ struct FlowArgs {
     const int *n_active;  // early termination: skip the launch once every frame converged
     unsigned long long *stats;  // optional instrumentation (QCL_FLOW_STATS)
     double clip, eps;
+    double mag_max;             // FP32 bound on |r| (LayerArgs::mag_max)
 };
 
 __host__ __device__ constexpr int flow_class_V(int cls) { return cls == 0 ? 4 : cls == 1 ? 2 : 1; }
@@ -154,8 +155,7 @@ __device__ __forceinline__ void flow_runs(const FlowArgs &a, const FlowHdr &h, c
 
 // One consumer thread: check (ci) of the tile for V lanes, in place in the stage.
 template <int V, int D, bool HAS_SYN>
-__device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
-                                             const LayerArgs &la) {
+__device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct) {
     const int W = 1 << a.lw;
     const int KT = kFlowConsumers * 32 * V / W;
     const int KTW = KT * W;
@@ -189,12 +189,114 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
             for (int v = 0; v < V; v++) q[j][v] = 0.0f;
         }
     }
-    check_update<V, D>(q, ph, par, h.d, la);
+    if (D == 4 && h.d == 4) {
+        uint32_t sb[V];
+#pragma unroll
+        for (int v = 0; v < V; v++) sb[v] = (uint32_t)par[v] << 31;
+        check_update_f32_d4<V>(reinterpret_cast<float(&)[4][V]>(q), reinterpret_cast<float(&)[4][V]>(ph), sb,
+                               (float)a.mag_max, clip);
+    } else {
+        check_update_f32<V, D>(q, ph, par, h.d, (float)a.mag_max, clip);
+    }
 #pragma unroll
     for (int j = 0; j < D; j++) {
         if (j < h.d) {
             *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(ph[j]);
             *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(q[j]);
+        }
+    }
+}
+
+// Degree classes 1 and 2 (rows of degree 5..12): the tanh-product update with the
+// exclusive prefix products stashed in the tile's own shared-memory slots of each edge
+// (free once the edge's L and R are in registers) instead of registers, so the 80-register
+// budget of two resident CTAs per SM holds without spills.  Same arithmetic, in the same
+// order, as check_update_f32.
+template <int V, int D, bool HAS_SYN>
+__device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHdr &h, float *stage, int ct) {
+    const int W = 1 << a.lw;
+    const int KT = kFlowConsumers * 32 * V / W;
+    const int KTW = KT * W;
+    const int lanes_v = W / V;
+    const int ci = ct / lanes_v;
+    const int w0 = (ct - ci * lanes_v) * V;
+    if (ci >= h.kt) return;
+    const int off = ci * W + w0;
+    const float clip = (float)a.clip, mag_max = (float)a.mag_max;
+    using VT = typename Vec<float, V>::type;
+    float q[D][V], c[D][V];
+    int par[V];
+    if (HAS_SYN) {
+        const uint8_t *sp = a.syn + ((((int64_t)h.g * a.S + h.slot) * a.z + h.k0 + ci) << a.lw) + w0;
+#pragma unroll
+        for (int v = 0; v < V; v++) par[v] = sp[v] & 1;
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; v++) par[v] = 0;
+    }
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+#pragma unroll
+        for (int v = 0; v < V; v++) c[j][v] = 0.0f;
+        if (j < h.d) {
+            float lv[V], rv[V];
+            *reinterpret_cast<VT *>(lv) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
+            *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+#pragma unroll
+            for (int v = 0; v < V; v++) {
+                q[j][v] = clampT(lv[v] - rv[v], clip);
+                float u_;
+                tanh_pair(q[j][v], u_, c[j][v]);
+                par[v] ^= (q[j][v] < 0.0f);
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < V; v++) q[j][v] = 0.0f;
+        }
+    }
+    // exclusive prefix products (u) and complements (1 - prod u) -> the edge's L / R slots
+    {
+        float pu[V], pc[V];
+#pragma unroll
+        for (int v = 0; v < V; v++) {
+            pu[v] = 1.0f;
+            pc[v] = 0.0f;
+        }
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            if (j < h.d) {
+                *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(pu);
+                *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(pc);
+#pragma unroll
+                for (int v = 0; v < V; v++) {
+                    pu[v] *= 1.0f - c[j][v];
+                    pc[v] = comp_mul(pc[v], c[j][v]);
+                }
+            }
+        }
+    }
+    float su[V], sc[V];
+#pragma unroll
+    for (int v = 0; v < V; v++) {
+        su[v] = 1.0f;
+        sc[v] = 0.0f;
+    }
+#pragma unroll
+    for (int j = D - 1; j >= 0; j--) {
+        if (j < h.d) {
+            float tu[V], tcv[V], rr[V], ll[V];
+            *reinterpret_cast<VT *>(tu) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
+            *reinterpret_cast<VT *>(tcv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+#pragma unroll
+            for (int v = 0; v < V; v++) {
+                const float mag = tanh_out(tu[v] * su[v], comp_mul(tcv[v], sc[v]), mag_max);
+                rr[v] = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
+                ll[v] = clampT(q[j][v] + rr[v], clip);
+                su[v] *= 1.0f - c[j][v];
+                sc[v] = comp_mul(sc[v], c[j][v]);
+            }
+            *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(rr);
+            *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(ll);
         }
     }
 }
@@ -206,7 +308,7 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
         tc = c_;                              \
     }
 
-template <bool HAS_SYN>
+template <bool HAS_SYN, bool PROF>
 __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
     if (a.n_active && *(volatile const int *)a.n_active == 0) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -240,7 +342,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const bool prof = a.stats != nullptr;
+    constexpr bool prof = PROF;  // instrumented build (QCL_FLOW_STATS): phase cycle counters
     long long acc[4] = {0, 0, 0, 0}, tc = 0;
 
     if (warp == 0) {
@@ -258,7 +360,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
         int sentinels = 0;
         for (int it = 0, q = 0, ph = 0;; it++) {
             if (prof) tc = clock64();
-            if (it >= kFlowQueue) mbar_wait(&qfree[q], ph ^ 1);
+            if (it >= kFlowQueue) mbar_wait_sleep(&qfree[q], ph ^ 1);
             FLOW_TICK(0);
             const int item = n1;
             const int2 e = r1;
@@ -335,7 +437,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
         const uint64_t pol_keep = policy_evict_last();
         int sentinels = 0;
         for (int it = 0, s = 0, ph = 0, q = 0, qph = 0;; it++) {
-            mbar_wait(&ready[q], qph);
+            mbar_wait_sleep(&ready[q], qph);
             const FlowHdr h = hq[q];
             __syncwarp();
             if (lane == 0) mbar_arrive(&qfree[q]);
@@ -343,7 +445,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
                 q = 0;
                 qph ^= 1;
             }
-            if (it >= S) mbar_wait(&empty[s], ph ^ 1);
+            if (it >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
             if (h.kt < 0) {
                 if (lane == 0) {
                     hdr[s].kt = -1;
@@ -375,11 +477,11 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
         // writes to complete overlaps the other's stores
         const uint64_t pol_stream = policy_evict_first();
         const uint64_t pol_keep = policy_evict_last();
-        const bool sprof = prof && warp == 2;
+        const bool sprof = PROF && warp == 2;
         for (int it = warp - 2;; it += kFlowStorers) {
             const int s = it % S;
             if (sprof) tc = clock64();
-            mbar_wait(&done[s], (it / S) & 1);
+            mbar_wait_sleep(&done[s], (it / S) & 1);
             if (sprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
             const FlowHdr h = hdr[s];
             if (h.kt < 0) break;
@@ -406,16 +508,11 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
 
     // ---------------------------------------------------------------------- consumers
     const int ct = threadIdx.x - 32 * (2 + kFlowStorers);
-    const bool cprof = prof && warp == 2 + kFlowStorers;
-    LayerArgs la;
-    la.uniform = 0;
-    la.clip_r = a.clip_r;
-    la.clip = a.clip;
-    la.eps = a.eps;
+    const bool cprof = PROF && warp == 2 + kFlowStorers;
     int sentinels = 0;
     for (int s = 0, ph = 0;;) {
         if (cprof) tc = clock64();
-        mbar_wait(&full[s], ph);
+        mbar_wait_sleep(&full[s], ph);
         if (cprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
         const FlowHdr h = hdr[s];
         if (h.kt < 0) {
@@ -424,11 +521,11 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
         } else {
             float *stage = stages + (size_t)s * kStageElems;
             if (h.cls == 0)
-                flow_consume<4, 4, HAS_SYN>(a, h, stage, ct, la);
+                flow_consume<4, 4, HAS_SYN>(a, h, stage, ct);
             else if (h.cls == 1)
-                flow_consume<2, 8, HAS_SYN>(a, h, stage, ct, la);
+                flow_consume_gen<2, 8, HAS_SYN>(a, h, stage, ct);
             else
-                flow_consume<1, 12, HAS_SYN>(a, h, stage, ct, la);
+                flow_consume_gen<1, 12, HAS_SYN>(a, h, stage, ct);
             fence_proxy_async_smem();  // this thread's STS -> visible to the bulk-store engine
             __syncwarp();
             if (lane == 0) mbar_arrive(&done[s]);

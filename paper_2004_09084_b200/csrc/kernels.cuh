@@ -60,6 +60,7 @@ struct LayerArgs {
     int32_t clip_r;      // the clip can bind |r| (clip < Phi(eps)); else the r clip is skipped
     const int *n_active; // early termination: skip the launch once every frame converged
     double clip, eps;
+    double mag_max;      // FP32 bound on |r|: min(Phi(eps), clip if clip_r)
 };
 
 template <typename T, int V> struct Vec;
@@ -203,88 +204,115 @@ __device__ __forceinline__ Item map_item(const SlotRange &r) {
     return it;
 }
 
-// FP32 check update of one check for V lanes (decoder.py:219-249), lean form:
-//   in:  q[j][v] = clip(L - r_old), d live edges, par[v] = syndrome bit
+// ---- FP32 check update: tanh-product form ----------------------------------------
+//
+// The reference computes r_j = +-Phi(sum_{i != j} Phi(|q_i|)) with Phi(x) = -ln tanh(x/2)
+// (decoder.py:225-245).  Since Phi(x) = -ln u with u = tanh(x/2), the same message is
+//     r_j = +-2 artanh(P_j),  P_j = prod_{i != j} u_i          (the tanh rule, i.e. the
+// reference test-suite's own check_node_oracle, tests/oracles.py:40-58),
+// and 2 artanh(P) = ln((1 + P) / (1 - P)).  FP32 evaluation:
+//   * per edge  e = 2^(|q| log2 e) (MUFU.EX2), d = 1 - u = 2 / (e + 1) (one FFMA + MUFU.RCP),
+//     u = 1 - d.  d is accurate to ~1 ulp where it is tiny (strong messages); u loses
+//     relative accuracy only where u is small, and there every message that depends on
+//     it is ~2P, so the error stays ~1e-7 ABSOLUTE;
+//   * exclusive products P_j (prefix/suffix FMULs) and their complements
+//     D_j = 1 - P_j folded as 1 - (1-a)(1-b) = a + b - ab (one FADD + one FFMA), so
+//     1 - P_j never cancels when every other message is strong and P_j ~ 1;
+//   * |r_j| = min(lg2((1 + P_j) / D_j) ln 2, mag_max) with mag_max = min(Phi(eps),
+//     clip if the clip binds r): the reference's clamp of `others` to >= eps
+//     (decoder.py:104) is exactly |r| <= Phi(eps) (Phi is decreasing and self-inverse);
+//     its upper clamp at `clip` moves |r| by < Phi(clip) = 1.9e-13.  An input |q| < eps
+//     gives u = 0, hence r = 0 on the other edges instead of Phi(Phi(eps)) = eps = 1e-10.
+// 4 MUFU and ~25 instructions per edge (the Phi-domain form needed 6 MUFU and ~37).
+// Signs: r_j = |r_j| with sign (q_j < 0) ^ parity(all q < 0) ^ syndrome bit.
+__device__ __forceinline__ void tanh_pair(float q, float &u, float &d) {
+    const float e = ex2_approx(fabsf(q) * 1.4426950408889634f);  // e^|q| (inf for |q| > 88: d = 0, u = 1)
+    d = rcp_approx(fmaf(e, 0.5f, 0.5f));
+    u = 1.0f - d;
+}
+__device__ __forceinline__ float comp_mul(float a, float b) { return fmaf(-a, b, a + b); }  // 1 - (1-a)(1-b)
+__device__ __forceinline__ float tanh_out(float P, float D, float mag_max) {
+    // D = 0 only when every other message is infinitely strong: lg2(inf) -> mag_max
+    return fminf(lg2_approx((1.0f + P) * rcp_approx(D)) * 0.6931471805599453f, mag_max);
+}
+
+// Any degree <= D (edges j >= d are neutral: u = 1, d = 0):
+//   in:  q[j][v] = clip(L - r_old), par[v] = syndrome bit
 //   out: q[j][v] <- new posterior clip(q + r), ph[j][v] <- new message r
-// ph_j = Phi(|q_j|) in log2 units (phi_in), exclusive prefix+suffix sums give others_j,
-// r_j = +-Phi(others_j) (phi_out) with sign (q_j < 0) ^ parity.
 template <int V, int D>
 __device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D][V], int (&par)[V], int d,
-                                                 float eps, float clip, bool clip_r) {
-    const float kInvLn2 = 1.4426950408889634f;
-#pragma unroll
-    for (int j = 0; j < D; j++) {
-#pragma unroll
-        for (int v = 0; v < V; v++) {
-            if (j < d) {
-                ph[j][v] = phi_in(fabsf(q[j][v]));
-                par[v] ^= (q[j][v] < 0.0f);
-            } else {
-                ph[j][v] = 0.0f;
-            }
-        }
-    }
+                                                 float mag_max, float clip) {
 #pragma unroll
     for (int v = 0; v < V; v++) {
-        float pre = 0.0f, suf = 0.0f, tmp[D];
+        // only d = 1 - u is kept per edge; u = 1 - d is recomputed (it is defined that way,
+        // so the values are identical) to keep the degree-12 variant in registers
+        float c[D];
 #pragma unroll
         for (int j = 0; j < D; j++) {
-            tmp[j] = pre;
-            pre += ph[j][v];
+            if (j < d) {
+                float u_;
+                tanh_pair(q[j][v], u_, c[j]);
+                par[v] ^= (q[j][v] < 0.0f);
+            } else {
+                c[j] = 0.0f;
+            }
         }
+        float pu = 1.0f, pc = 0.0f, tu[D], tc[D];
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            tu[j] = pu;
+            tc[j] = pc;
+            pu *= 1.0f - c[j];
+            pc = comp_mul(pc, c[j]);
+        }
+        float su = 1.0f, sc = 0.0f;
 #pragma unroll
         for (int j = D - 1; j >= 0; j--) {
-            const float p = ph[j][v];
-            ph[j][v] = tmp[j] + suf;
-            suf += p;
-        }
-    }
-    const float lo2 = eps * kInvLn2;
-#pragma unroll
-    for (int j = 0; j < D; j++) {
-#pragma unroll
-        for (int v = 0; v < V; v++) {
             if (j < d) {
-                float mag = phi_out(fmaxf(ph[j][v], lo2));
-                if (clip_r) mag = fminf(mag, clip);
+                const float mag = tanh_out(tu[j] * su, comp_mul(tc[j], sc), mag_max);
                 const float r = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
                 ph[j][v] = r;
                 q[j][v] = clampT(q[j][v] + r, clip);
             }
+            su *= 1.0f - c[j];
+            sc = comp_mul(sc, c[j]);
         }
     }
 }
 
-// Exact-degree-4 FP32 update (the 350 rows of type 3+1 that dominate the MET code):
-// no predication, six adds for the four exclusive sums, and signs handled as IEEE sign
-// bits: parity = XOR of the q sign bits (^ syndrome), r = |Phi(others)| | (sign(q) ^
-// parity).  Exact because the FP32 state never holds -0.0 (reset/upload canonicalise
-// it, |r| > 0 so q + r != -0.0 and L - r_old != -0.0), so sign bit == (q < 0).
+// Exact degree 4 (the 350 rows of type 3+1 that dominate the MET code): no predication,
+// 6 FMULs + 6 complement folds for the exclusive products, and signs handled as IEEE sign
+// bits: parity = XOR of the q sign bits (^ syndrome), r = |r| | (sign(q) ^ parity).
+// Exact because the FP32 state never holds -0.0 (reset/upload canonicalise it, r != -0.0
+// and q + r, L - r_old are never -0.0 for finite nonzero operands of equal magnitude
+// under round-to-nearest), so sign bit == (q < 0).
 template <int V>
 __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph)[4][V], const uint32_t (&synbit)[V],
-                                                    float eps, float clip, bool clip_r) {
-    const float kInvLn2 = 1.4426950408889634f;
-    const float lo2 = eps * kInvLn2;
+                                                    float mag_max, float clip) {
 #pragma unroll
     for (int v = 0; v < V; v++) {
         uint32_t qs[4];
-        float p[4];
+        float u[4], c[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             qs[j] = __float_as_uint(q[j][v]) & 0x80000000u;
-            p[j] = phi_in(fabsf(q[j][v]));
+            tanh_pair(q[j][v], u[j], c[j]);
         }
         const uint32_t par = qs[0] ^ qs[1] ^ qs[2] ^ qs[3] ^ synbit[v];
-        const float c = p[0] + p[1], b = p[2] + p[3];
-        float o[4];
-        o[0] = p[1] + b;
-        o[1] = p[0] + b;
-        o[2] = c + p[3];
-        o[3] = c + p[2];
+        const float u01 = u[0] * u[1], u23 = u[2] * u[3];
+        const float c01 = comp_mul(c[0], c[1]), c23 = comp_mul(c[2], c[3]);
+        float P[4], C[4];
+        P[0] = u[1] * u23;
+        P[1] = u[0] * u23;
+        P[2] = u01 * u[3];
+        P[3] = u01 * u[2];
+        C[0] = comp_mul(c[1], c23);
+        C[1] = comp_mul(c[0], c23);
+        C[2] = comp_mul(c01, c[3]);
+        C[3] = comp_mul(c01, c[2]);
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            float mag = phi_out(fmaxf(o[j], lo2));
-            if (clip_r) mag = fminf(mag, clip);
+            const float mag = tanh_out(P[j], C[j], mag_max);
             const float r = __uint_as_float(__float_as_uint(mag) | (qs[j] ^ par));
             ph[j][v] = r;
             q[j][v] = clampT(q[j][v] + r, clip);
@@ -331,11 +359,11 @@ __device__ __forceinline__ void check_update(float (&q)[D][V], float (&ph)[D][V]
             uint32_t sb[V];
 #pragma unroll
             for (int v = 0; v < V; v++) sb[v] = (uint32_t)par[v] << 31;
-            check_update_f32_d4<V>(q, ph, sb, (float)a.eps, (float)a.clip, a.clip_r != 0);
+            check_update_f32_d4<V>(q, ph, sb, (float)a.mag_max, (float)a.clip);
             return;
         }
     }
-    check_update_f32<V, D>(q, ph, par, d, (float)a.eps, (float)a.clip, a.clip_r != 0);
+    check_update_f32<V, D>(q, ph, par, d, (float)a.mag_max, (float)a.clip);
 }
 template <int V, int D>
 __device__ __forceinline__ void check_update(double (&q)[D][V], double (&ph)[D][V], int (&par)[V], int d,

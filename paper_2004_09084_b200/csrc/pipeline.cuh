@@ -52,6 +52,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Same wait with a suspend-time hint: the warp sleeps in the barrier unit until the phase
+// completes (or the hint elapses) instead of re-issuing try_wait, so idle roles (flow
+// engine) leave their issue slots to the consumer warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(1000000)
+        : "memory");
+}
 __device__ __forceinline__ void bulk_load(void *smem_dst, const void *gmem_src, uint32_t bytes, uint64_t *bar,
                                           uint64_t policy) {
     asm volatile(
@@ -104,6 +118,7 @@ struct PipeArgs {
     int32_t clip_r;
     const int *n_active;  // early termination: skip the launch once every frame converged
     double clip, eps;
+    double mag_max;       // FP32 bound on |r| (LayerArgs::mag_max)
 };
 
 struct TileGeom {
@@ -239,6 +254,7 @@ __global__ void __launch_bounds__(32 * (C + 1), (pipe_min_blocks<T, V, D, C>()))
     la.clip_r = a.clip_r;
     la.clip = a.clip;
     la.eps = a.eps;
+    la.mag_max = a.mag_max;
     const T clip = (T)a.clip;
     using VT = typename Vec<T, V>::type;
     int it = 0;

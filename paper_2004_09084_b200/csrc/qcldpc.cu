@@ -47,6 +47,10 @@ static int fail(int code, const char *fmt, ...) {
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// FP32 bound on |r|: Phi(eps) (the reference clamps `others` to >= eps, decoder.py:104),
+// and the clip where it binds (decoder.py:244-245).
+static double mag_bound(double clip, double eps) { return std::min(clip, log1p(2.0 / expm1(eps))); }
+
 struct qcl_plan {
     int device = 0;
     int z = 0, n_cols = 0, S = 0, n_layers = 0, E = 0;
@@ -287,6 +291,7 @@ static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_
     a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));
     a.clip = clip;
     a.eps = eps;
+    a.mag_max = mag_bound(clip, eps);
     if (st->prec == QCL_PREC_FP32)
         launch_tma<float>(a, V, u.dmax, stream, st->has_syn);
     else
@@ -314,6 +319,7 @@ static void enqueue_unit(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t st
     a.n_active = st->g_et ? st->n_active : nullptr;
     a.clip = clip;
     a.eps = eps;
+    a.mag_max = mag_bound(clip, eps);
     dim3 grid((unsigned)((int64_t)ng * a.r.nslots * a.r.bps));
     if (st->prec == QCL_PREC_FP32) {
         if (V == 4)
@@ -443,9 +449,10 @@ static int ensure_flow(qcl_state *st, int counters) {
             return QCL_OK;
         }
         st->f_stages = stages;
-        for (auto kern : {flow_kernel<false>, flow_kernel<true>})
+        for (auto kern : {flow_kernel<false, false>, flow_kernel<true, false>, flow_kernel<false, true>,
+                          flow_kernel<true, true>})
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<false>, kFlowThreads, smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<false, false>, kFlowThreads, smem));
         st->f_grid = sms * std::max(1, per_sm);
     }
     if (st->f_counter_cap < counters) {
@@ -494,12 +501,14 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.stats = st->fstats;
     a.clip = clip;
     a.eps = eps;
+    a.mag_max = mag_bound(clip, eps);
     const size_t smem = flow_smem_bytes(p->S, p->E, st->f_stages);
     const int64_t grid = std::min<int64_t>(st->f_grid, a.item_end - a.item_begin);
+    const bool prof = st->fstats != nullptr;
     if (st->has_syn)
-        flow_kernel<true><<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
+        (prof ? flow_kernel<true, true> : flow_kernel<true, false>)<<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
     else
-        flow_kernel<false><<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
+        (prof ? flow_kernel<false, true> : flow_kernel<false, false>)<<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
     CK(cudaGetLastError());
     st->launches_layer++;
     st->launches_all++;

@@ -11,11 +11,15 @@ concurrently.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
 
 LIB_PATH = Path(__file__).resolve().parent / "libqcldpc_b200.so"
+# tuning runs (tools/flow_build_variants.sh) may point at an in-tree variant build
+if os.environ.get("QCL_LIB_VARIANT"):
+    LIB_PATH = LIB_PATH.with_name(f"libqcldpc_b200_{os.environ['QCL_LIB_VARIANT']}.so")
 
 QCL_OK, QCL_EVALUE, QCL_ECUDA, QCL_EUNSUP = 0, -1, -2, -3
 PREC = {"fp32": 0, "fp64": 1}

@@ -41,12 +41,19 @@
 
 #include "pipeline.cuh"
 
+#ifndef QCL_FLOW_QUEUE
+#define QCL_FLOW_QUEUE 2
+#endif
+#ifndef QCL_FLOW_CLAIM_AHEAD
+#define QCL_FLOW_CLAIM_AHEAD 1
+#endif
+
 namespace qcl {
 
 constexpr int kFlowConsumers = 8;                  // consumer warps per CTA
 constexpr int kFlowStorers = 2;                    // storer warps per CTA
 constexpr int kFlowThreads = 32 * (kFlowConsumers + 2 + kFlowStorers);
-constexpr int kFlowQueue = 4;                      // scheduler -> loader header queue
+constexpr int kFlowQueue = QCL_FLOW_QUEUE;         // scheduler -> loader header queue depth
 constexpr int kFlowStageBytes = 32 * 1024;         // 2*D*KT*W*4 <= 32 KB for every class
 constexpr int kFlowMaxStages = 4;
 constexpr int kFlowHeadBytes = 512;                // mbarriers + stage headers + header queue
@@ -351,13 +358,18 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
         // trip is on the tile's critical path.  Holding claimed items is deadlock free:
         // they are larger than the item in hand.  Resolved headers go to the loader warp
         // through a small queue, so dependency polling overlaps the bulk-copy issue.
-        int n2 = 0;
+        int n2 = 0, n3 = 0;
         if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
         int n1 = __shfl_sync(0xffffffffu, n2, 0);
         int2 r1 = make_int2(0, 0);
         if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
         if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
+        if (QCL_FLOW_CLAIM_AHEAD == 2) {  // n2: the item after n1 (broadcast); n3: claim in flight
+            n2 = __shfl_sync(0xffffffffu, n2, 0);
+            if (lane == 0) n3 = a.item_begin + atomicAdd(a.counter, 1);
+        }
         int sentinels = 0;
+        unsigned long long n_waited = 0, n_polls = 0, n_tiles = 0;
         for (int it = 0, q = 0, ph = 0;; it++) {
             if (prof) tc = clock64();
             if (it >= kFlowQueue) mbar_wait_sleep(&qfree[q], ph ^ 1);
@@ -372,9 +384,16 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
                 }
                 if (++sentinels == kFlowStorers) break;
             } else {
-                n1 = __shfl_sync(0xffffffffu, n2, 0);
-                if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
-                if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
+                if (QCL_FLOW_CLAIM_AHEAD == 2) {
+                    n1 = n2;
+                    if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
+                    n2 = __shfl_sync(0xffffffffu, n3, 0);
+                    if (lane == 0) n3 = a.item_begin + atomicAdd(a.counter, 1);
+                } else {
+                    n1 = __shfl_sync(0xffffffffu, n2, 0);
+                    if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
+                    if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
+                }
                 FLOW_TICK(1);
                 FlowHdr h;
                 h.t = item / a.sweep_items;
@@ -408,11 +427,9 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
                 FLOW_TICK(2);
                 if (prof) {
                     polls = __reduce_add_sync(0xffffffffu, polls);
-                    if (lane == 0) {
-                        if (polls) atomicAdd(a.stats, 1ull);
-                        atomicAdd(a.stats + 1, (unsigned long long)polls);
-                        atomicAdd(a.stats + 2, 1ull);
-                    }
+                    n_waited += polls != 0;
+                    n_polls += polls;
+                    n_tiles++;
                 }
                 __syncwarp();
                 if (lane == 0) {
@@ -426,8 +443,12 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
                 ph ^= 1;
             }
         }
-        if (prof && lane == 0)
+        if (prof && lane == 0) {
             for (int k = 0; k < 4; k++) atomicAdd(a.stats + 3 + k, (unsigned long long)acc[k]);
+            atomicAdd(a.stats, n_waited);
+            atomicAdd(a.stats + 1, n_polls);
+            atomicAdd(a.stats + 2, n_tiles);
+        }
         return;
     }
 
@@ -502,7 +523,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
             if (sprof) acc[3] += clock64() - tc;
         }
         if (sprof && lane == 0)
-            for (int k = 0; k < 4; k++) atomicAdd(a.stats + 9 + k, (unsigned long long)acc[k]);
+            for (int k = 0; k < 4; k++) atomicAdd(a.stats + 11 + k, (unsigned long long)acc[k]);
         return;
     }
 
@@ -537,7 +558,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
         }
     }
     if (cprof && lane == 0)
-        for (int k = 0; k < 2; k++) atomicAdd(a.stats + 7 + k, (unsigned long long)acc[k]);
+        for (int k = 0; k < 2; k++) atomicAdd(a.stats + 9 + k, (unsigned long long)acc[k]);
 }
 #undef FLOW_TICK
 

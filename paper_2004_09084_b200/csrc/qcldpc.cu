@@ -436,6 +436,9 @@ static int ensure_flow(qcl_state *st, int counters) {
             CK(cudaMalloc(&st->fstats, 16 * sizeof(unsigned long long)));
             CK(cudaMemset(st->fstats, 0, 16 * sizeof(unsigned long long)));
         }
+        // cudaMemcpy from pageable memory may return before its DMA lands, and the state's
+        // stream does not synchronise with the legacy stream: wait for the uploads here
+        CK(cudaDeviceSynchronize());
         // ring depth: QCL_FLOW_STAGES (default 3), reduced until two CTAs fit per SM
         static int want = env_int("QCL_FLOW_STAGES", 3);
         int stages = std::max(2, std::min(want, kFlowMaxStages));
@@ -754,6 +757,10 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
         e = cudaMemcpy(p->slots, p->h_slots.data(), sizeof(SlotInfo) * n_slots, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->edges, h_edges.data(), sizeof(EdgeInfo) * n_edges, cudaMemcpyHostToDevice);
+    // the uploads above may still be in flight (pageable-source cudaMemcpy returns once the
+    // data is staged), and states run on non-blocking streams: the plan is immutable after
+    // this point, so wait for it once
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         cudaFree(p->slots);
         cudaFree(p->edges);
@@ -792,9 +799,12 @@ int qcl_plan_info(const qcl_plan *p, int64_t *n_vars, int64_t *n_checks, int64_t
 }
 
 static int lanes_log2(int64_t B) {
-    // W = min(32, next pow2 >= B); override with QCL_LANES for tuning
+    // W = min(8, next pow2 >= B): 8 lanes (32-byte FP32 runs, still whole 16-byte bulk-copy
+    // units) give the flow engine 8 independent lane groups per 64 codewords, i.e. more
+    // slack between a tile and the previous-layer tiles it waits for (tools/flow_grid.sh:
+    // 25.7 ms at W = 8 vs 26.6 ms at W = 32 per 64-codeword decode); override: QCL_LANES
     const char *env = getenv("QCL_LANES");
-    int want = env ? atoi(env) : 32;
+    int want = env ? atoi(env) : 8;
     int lw = 0;
     while ((1 << lw) < B && (1 << lw) < want && lw < 5) lw++;
     return lw;
@@ -864,11 +874,11 @@ int qcl_state_destroy(qcl_state *st) {
         fprintf(stderr, "[flow stats] B=%lld W=%d tiles=%llu waited=%llu (%.2f%%) polls=%llu\n", (long long)st->B,
                 st->W, h[2], h[0], h[2] ? 100.0 * h[0] / h[2] : 0.0, h[1]);
         const double T = h[2] ? (double)h[2] : 1.0;
-        fprintf(stderr, "[flow stats] cycles/tile scheduler: qfree %.0f claim %.0f deps %.0f queue %.0f | "
-                        "consumer: full-wait %.0f compute %.0f | storer(x2 tiles): done-wait %.0f issue %.0f "
-                        "read %.0f write+release %.0f\n",
-                h[3] / T, h[4] / T, h[5] / T, h[6] / T, h[7] / T, h[8] / T, 2 * h[9] / T, 2 * h[10] / T,
-                2 * h[11] / T, 2 * h[12] / T);
+        fprintf(stderr, "[flow stats] cycles/tile scheduler: qfree %.0f claim %.0f deps %.0f queue %.0f | consumer: "
+                        "full-wait %.0f compute %.0f | storer(x2 tiles): done-wait %.0f issue %.0f read %.0f "
+                        "write+release %.0f\n",
+                h[3] / T, h[4] / T, h[5] / T, h[6] / T, h[9] / T, h[10] / T, 2 * h[11] / T, 2 * h[12] / T,
+                2 * h[13] / T, 2 * h[14] / T);
     }
     if (st->sweep_exec) cudaGraphExecDestroy(st->sweep_exec);
     if (st->decode_exec) cudaGraphExecDestroy(st->decode_exec);

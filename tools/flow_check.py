@@ -62,11 +62,11 @@ def decodes_equal(name, batch, iters, et, snr):
     return same
 
 
-def timing(batch=64, iters=50):
+def timing(batch=64, iters=50, engines=(0, 4)):
     base, sched, index = code("standin_v2_z2500")
     plan = _native.Plan(index, sched, 0)
     n = base.n_cols * base.z
-    for engine in (0, 4):
+    for engine in engines:
         st = _native.State(plan, batch, "fp32")
         st.set_engine(engine)
         st.set_llr_synthetic(seed=0, snr_idx=0, first_frame=0, snr=0.161)

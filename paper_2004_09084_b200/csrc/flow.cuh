@@ -214,8 +214,8 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
     }
 }
 
-// Degree classes 1 and 2 (rows of degree 5..12): the tanh-product update with the
-// exclusive prefix products stashed in the tile's own shared-memory slots of each edge
+// Degree classes 1 and 2 (rows of degree 5..12): the sum/difference update with the
+// exclusive prefix (S, D) pairs stashed in the tile's own shared-memory slots of each edge
 // (free once the edge's L and R are in registers) instead of registers, so the 80-register
 // budget of two resident CTAs per SM holds without spills.  Same arithmetic, in the same
 // order, as check_update_f32.
@@ -231,7 +231,7 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
     const int off = ci * W + w0;
     const float clip = (float)a.clip, mag_max = (float)a.mag_max;
     using VT = typename Vec<float, V>::type;
-    float q[D][V], c[D][V];
+    float q[D][V], t[D][V];
     int par[V];
     if (HAS_SYN) {
         const uint8_t *sp = a.syn + ((((int64_t)h.g * a.S + h.slot) * a.z + h.k0 + ci) << a.lw) + w0;
@@ -244,7 +244,10 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
 #pragma unroll
     for (int j = 0; j < D; j++) {
 #pragma unroll
-        for (int v = 0; v < V; v++) c[j][v] = 0.0f;
+        for (int v = 0; v < V; v++) {
+            q[j][v] = 0.0f;
+            t[j][v] = 0.0f;
+        }
         if (j < h.d) {
             float lv[V], rv[V];
             *reinterpret_cast<VT *>(lv) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
@@ -252,55 +255,54 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
 #pragma unroll
             for (int v = 0; v < V; v++) {
                 q[j][v] = clampT(lv[v] - rv[v], clip);
-                float u_;
-                tanh_pair(q[j][v], u_, c[j][v]);
+                t[j][v] = sd_t(q[j][v]);
                 par[v] ^= (q[j][v] < 0.0f);
             }
-        } else {
-#pragma unroll
-            for (int v = 0; v < V; v++) q[j][v] = 0.0f;
         }
     }
-    // exclusive prefix products (u) and complements (1 - prod u) -> the edge's L / R slots
+    // exclusive prefix (S, D) pairs -> the edge's L / R slots
     {
-        float pu[V], pc[V];
+        float ps[V], pd[V];
 #pragma unroll
         for (int v = 0; v < V; v++) {
-            pu[v] = 1.0f;
-            pc[v] = 0.0f;
+            ps[v] = 1.0f;
+            pd[v] = 0.0f;
         }
 #pragma unroll
         for (int j = 0; j < D; j++) {
             if (j < h.d) {
-                *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(pu);
-                *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(pc);
+                *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(ps);
+                *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(pd);
 #pragma unroll
                 for (int v = 0; v < V; v++) {
-                    pu[v] *= 1.0f - c[j][v];
-                    pc[v] = comp_mul(pc[v], c[j][v]);
+                    const float ns = fmaf(t[j][v], pd[v], ps[v]);
+                    pd[v] = fmaf(t[j][v], ps[v], pd[v]);
+                    ps[v] = ns;
                 }
             }
         }
     }
-    float su[V], sc[V];
+    float ss[V], sd[V];
 #pragma unroll
     for (int v = 0; v < V; v++) {
-        su[v] = 1.0f;
-        sc[v] = 0.0f;
+        ss[v] = 1.0f;
+        sd[v] = 0.0f;
     }
 #pragma unroll
     for (int j = D - 1; j >= 0; j--) {
         if (j < h.d) {
-            float tu[V], tcv[V], rr[V], ll[V];
-            *reinterpret_cast<VT *>(tu) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
-            *reinterpret_cast<VT *>(tcv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+            float xs[V], xd[V], rr[V], ll[V];
+            *reinterpret_cast<VT *>(xs) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
+            *reinterpret_cast<VT *>(xd) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
 #pragma unroll
             for (int v = 0; v < V; v++) {
-                const float mag = tanh_out(tu[v] * su[v], comp_mul(tcv[v], sc[v]), mag_max);
+                const float S = fmaf(xs[v], ss[v], xd[v] * sd[v]), Dv = fmaf(xs[v], sd[v], xd[v] * ss[v]);
+                const float mag = sd_mag(S, Dv, mag_max);
                 rr[v] = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
                 ll[v] = clampT(q[j][v] + rr[v], clip);
-                su[v] *= 1.0f - c[j][v];
-                sc[v] = comp_mul(sc[v], c[j][v]);
+                const float ns = fmaf(t[j][v], sd[v], ss[v]);
+                sd[v] = fmaf(t[j][v], ss[v], sd[v]);
+                ss[v] = ns;
             }
             *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(rr);
             *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(ll);

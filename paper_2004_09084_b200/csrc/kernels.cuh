@@ -204,39 +204,35 @@ __device__ __forceinline__ Item map_item(const SlotRange &r) {
     return it;
 }
 
-// ---- FP32 check update: tanh-product form ----------------------------------------
+// ---- FP32 check update: tanh rule in sum/difference form -----------------------------
 //
 // The reference computes r_j = +-Phi(sum_{i != j} Phi(|q_i|)) with Phi(x) = -ln tanh(x/2)
-// (decoder.py:225-245).  Since Phi(x) = -ln u with u = tanh(x/2), the same message is
-//     r_j = +-2 artanh(P_j),  P_j = prod_{i != j} u_i          (the tanh rule, i.e. the
-// reference test-suite's own check_node_oracle, tests/oracles.py:40-58),
-// and 2 artanh(P) = ln((1 + P) / (1 - P)).  FP32 evaluation:
-//   * per edge  e = 2^(|q| log2 e) (MUFU.EX2), d = 1 - u = 2 / (e + 1) (one FFMA + MUFU.RCP),
-//     u = 1 - d.  d is accurate to ~1 ulp where it is tiny (strong messages); u loses
-//     relative accuracy only where u is small, and there every message that depends on
-//     it is ~2P, so the error stays ~1e-7 ABSOLUTE;
-//   * exclusive products P_j (prefix/suffix FMULs) and their complements
-//     D_j = 1 - P_j folded as 1 - (1-a)(1-b) = a + b - ab (one FADD + one FFMA), so
-//     1 - P_j never cancels when every other message is strong and P_j ~ 1;
-//   * |r_j| = min(lg2((1 + P_j) / D_j) ln 2, mag_max) with mag_max = min(Phi(eps),
-//     clip if the clip binds r): the reference's clamp of `others` to >= eps
-//     (decoder.py:104) is exactly |r| <= Phi(eps) (Phi is decreasing and self-inverse);
-//     its upper clamp at `clip` moves |r| by < Phi(clip) = 1.9e-13.  An input |q| < eps
-//     gives u = 0, hence r = 0 on the other edges instead of Phi(Phi(eps)) = eps = 1e-10.
-// 4 MUFU and ~25 instructions per edge (the Phi-domain form needed 6 MUFU and ~37).
+// (decoder.py:225-245).  With u_i = tanh(|q_i|/2) this is the tanh rule (the reference
+// test-suite's own check_node_oracle, tests/oracles.py:40-58):
+//     |r_j| = 2 artanh(P_j) = ln((1 + P_j) / (1 - P_j)),   P_j = prod_{i != j} u_i.
+// Write u_i = (1 - t_i) / (1 + t_i) with t_i = e^{-|q_i|} and, for a set X of edges,
+//     A_X = prod (1 + t_i),  B_X = prod (1 - t_i),  S_X = A_X + B_X,  D_X = A_X - B_X,
+// so that (1 + P_X) / (1 - P_X) = S_X / D_X.  Up to a common factor 2 (which cancels),
+// a single edge is (S, D) = (1, t) and two disjoint sets combine as
+//     S = S_X S_Y + D_X D_Y,   D = S_X D_Y + D_X S_Y        (one FMUL + one FFMA each),
+// i.e. adding one edge is S' = S + t D, D' = D + t S (two FFMAs).  Every term is
+// non-negative: no cancellation anywhere, so D keeps full relative accuracy when every
+// other message is strong (D ~ sum t_i, tiny) and S / D -> 1 stays accurate in absolute
+// terms when one is weak.  FP32 evaluation per edge: t = 2^(-|q| log2 e) (MUFU.EX2), and
+// per output |r_j| = min(lg2(S_j / D_j) ln 2, mag_max) (MUFU.RCP + MUFU.LG2), with
+// mag_max = min(Phi(eps), clip if the clip binds r): the reference's clamp of `others` to
+// >= eps (decoder.py:104) is exactly |r| <= Phi(eps) (Phi is decreasing and self-
+// inverse); its upper clamp at `clip` moves |r| by < Phi(clip) = 1.9e-13.  An input
+// |q| < eps gives t = 1, i.e. S = D and r = 0 on the other edges instead of eps = 1e-10.
+// 3 MUFU and ~19 instructions per edge (the Phi-domain form needed 6 MUFU and ~37).
 // Signs: r_j = |r_j| with sign (q_j < 0) ^ parity(all q < 0) ^ syndrome bit.
-__device__ __forceinline__ void tanh_pair(float q, float &u, float &d) {
-    const float e = ex2_approx(fabsf(q) * 1.4426950408889634f);  // e^|q| (inf for |q| > 88: d = 0, u = 1)
-    d = rcp_approx(fmaf(e, 0.5f, 0.5f));
-    u = 1.0f - d;
-}
-__device__ __forceinline__ float comp_mul(float a, float b) { return fmaf(-a, b, a + b); }  // 1 - (1-a)(1-b)
-__device__ __forceinline__ float tanh_out(float P, float D, float mag_max) {
+__device__ __forceinline__ float sd_t(float q) { return ex2_approx(fabsf(q) * -1.4426950408889634f); }
+__device__ __forceinline__ float sd_mag(float S, float D, float mag_max) {
     // D = 0 only when every other message is infinitely strong: lg2(inf) -> mag_max
-    return fminf(lg2_approx((1.0f + P) * rcp_approx(D)) * 0.6931471805599453f, mag_max);
+    return fminf(lg2_approx(S * rcp_approx(D)) * 0.6931471805599453f, mag_max);
 }
 
-// Any degree <= D (edges j >= d are neutral: u = 1, d = 0):
+// Any degree <= D (edges j >= d are neutral: t = 0, the identity (1, 0) of the combine):
 //   in:  q[j][v] = clip(L - r_old), par[v] = syndrome bit
 //   out: q[j][v] <- new posterior clip(q + r), ph[j][v] <- new message r
 template <int V, int D>
@@ -244,75 +240,75 @@ __device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D
                                                  float mag_max, float clip) {
 #pragma unroll
     for (int v = 0; v < V; v++) {
-        // only d = 1 - u is kept per edge; u = 1 - d is recomputed (it is defined that way,
-        // so the values are identical) to keep the degree-12 variant in registers
-        float c[D];
+        float t[D];
 #pragma unroll
         for (int j = 0; j < D; j++) {
             if (j < d) {
-                float u_;
-                tanh_pair(q[j][v], u_, c[j]);
+                t[j] = sd_t(q[j][v]);
                 par[v] ^= (q[j][v] < 0.0f);
             } else {
-                c[j] = 0.0f;
+                t[j] = 0.0f;
             }
         }
-        float pu = 1.0f, pc = 0.0f, tu[D], tc[D];
+        float ps = 1.0f, pd = 0.0f, xs[D], xd[D];  // exclusive prefixes
 #pragma unroll
         for (int j = 0; j < D; j++) {
-            tu[j] = pu;
-            tc[j] = pc;
-            pu *= 1.0f - c[j];
-            pc = comp_mul(pc, c[j]);
+            xs[j] = ps;
+            xd[j] = pd;
+            const float ns = fmaf(t[j], pd, ps);
+            pd = fmaf(t[j], ps, pd);
+            ps = ns;
         }
-        float su = 1.0f, sc = 0.0f;
+        float ss = 1.0f, sd = 0.0f;  // running suffix
 #pragma unroll
         for (int j = D - 1; j >= 0; j--) {
             if (j < d) {
-                const float mag = tanh_out(tu[j] * su, comp_mul(tc[j], sc), mag_max);
+                const float S = fmaf(xs[j], ss, xd[j] * sd), Dv = fmaf(xs[j], sd, xd[j] * ss);
+                const float mag = sd_mag(S, Dv, mag_max);
                 const float r = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
                 ph[j][v] = r;
                 q[j][v] = clampT(q[j][v] + r, clip);
             }
-            su *= 1.0f - c[j];
-            sc = comp_mul(sc, c[j]);
+            const float ns = fmaf(t[j], sd, ss);
+            sd = fmaf(t[j], ss, sd);
+            ss = ns;
         }
     }
 }
 
-// Exact degree 4 (the 350 rows of type 3+1 that dominate the MET code): no predication,
-// 6 FMULs + 6 complement folds for the exclusive products, and signs handled as IEEE sign
-// bits: parity = XOR of the q sign bits (^ syndrome), r = |r| | (sign(q) ^ parity).
-// Exact because the FP32 state never holds -0.0 (reset/upload canonicalise it, r != -0.0
-// and q + r, L - r_old are never -0.0 for finite nonzero operands of equal magnitude
-// under round-to-nearest), so sign bit == (q < 0).
+// Exact degree 4 (the 350 rows of type 3+1 that dominate the MET code): 12 FP32 ops for
+// the four exclusive (S, D) pairs, no predication, and signs handled as IEEE sign bits:
+// parity = XOR of the q sign bits (^ syndrome), r = |r| | (sign(q) ^ parity).  Exact
+// because the FP32 state never holds -0.0 (reset/upload canonicalise it; r != -0.0 and,
+// under round-to-nearest, q + r and L - r_old are -0.0 only for -0.0 operands), so the
+// sign bit == (q < 0).  Lane pairs use the packed FP32 instructions (FFMA2/FADD2/FMUL2).
 template <int V>
 __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph)[4][V], const uint32_t (&synbit)[V],
                                                     float mag_max, float clip) {
 #pragma unroll
     for (int v = 0; v < V; v++) {
         uint32_t qs[4];
-        float u[4], c[4];
+        float t[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             qs[j] = __float_as_uint(q[j][v]) & 0x80000000u;
-            tanh_pair(q[j][v], u[j], c[j]);
+            t[j] = sd_t(q[j][v]);
         }
         const uint32_t par = qs[0] ^ qs[1] ^ qs[2] ^ qs[3] ^ synbit[v];
-        const float u01 = u[0] * u[1], u23 = u[2] * u[3];
-        const float c01 = comp_mul(c[0], c[1]), c23 = comp_mul(c[2], c[3]);
-        float P[4], C[4];
-        P[0] = u[1] * u23;
-        P[1] = u[0] * u23;
-        P[2] = u01 * u[3];
-        P[3] = u01 * u[2];
-        C[0] = comp_mul(c[1], c23);
-        C[1] = comp_mul(c[0], c23);
-        C[2] = comp_mul(c01, c[3]);
-        C[3] = comp_mul(c01, c[2]);
+        const float S01 = fmaf(t[0], t[1], 1.0f), D01 = t[0] + t[1];
+        const float S23 = fmaf(t[2], t[3], 1.0f), D23 = t[2] + t[3];
+        float S[4], Dv[4];
+        S[0] = fmaf(t[1], D23, S23);
+        Dv[0] = fmaf(t[1], S23, D23);
+        S[1] = fmaf(t[0], D23, S23);
+        Dv[1] = fmaf(t[0], S23, D23);
+        S[2] = fmaf(t[3], D01, S01);
+        Dv[2] = fmaf(t[3], S01, D01);
+        S[3] = fmaf(t[2], D01, S01);
+        Dv[3] = fmaf(t[2], S01, D01);
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            const float mag = tanh_out(P[j], C[j], mag_max);
+            const float mag = sd_mag(S[j], Dv[j], mag_max);
             const float r = __uint_as_float(__float_as_uint(mag) | (qs[j] ^ par));
             ph[j][v] = r;
             q[j][v] = clampT(q[j][v] + r, clip);

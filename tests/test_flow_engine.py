@@ -1,0 +1,95 @@
+"""The flow engine (engine 4: one persistent launch per decode, tiles ordered by
+per-tile completion flags, csrc/flow.cuh) against the per-layer engine (0).
+
+Both engines run the same FP32 check-node arithmetic on the same tiles, so with the
+layer order preserved by the flags the results must be BIT-IDENTICAL: any missing
+dependency edge or memory-ordering hole shows up as a mismatch.  Decodes are repeated
+(the schedule is dynamic, so every run interleaves tiles differently) and start from
+fresh states (the upload path that once raced with the first launch).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, channel_llrs, load_code
+
+pytestmark = pytest.mark.gpu
+
+
+def _states(name, batch, seed=3, syndrome=False):
+    from paper_2004_09084_b200 import _native
+
+    base, sched, index = load_code(name)
+    plan = _native.Plan(index, sched, 0)
+    out = []
+    m = base.n_rows * base.z
+    syn = None
+    if syndrome:
+        syn = (np.random.default_rng(seed).random((batch, m)) < 0.5).astype(np.uint8)
+    for engine in (0, 4):
+        st = _native.State(plan, batch, "fp32")
+        st.set_engine(engine)
+        st.set_llr_synthetic(seed=seed, snr_idx=0, first_frame=0, snr=0.161)
+        st.set_syndrome(syn)
+        out.append(st)
+    return base, sched, out
+
+
+@pytest.mark.parametrize("name,batch,iters", [("standin_v2_z100", 64, 20), ("standin_v2_z2500", 64, 4),
+                                              ("standin_v2_z100", 8, 30), ("demo_6x12_z16", 33, 12)])
+def test_flow_decode_bit_identical_to_layer_engine(gpu, name, batch, iters):
+    import paper_2004_09084_b200 as q
+    from paper_2004_09084_b200 import _native
+
+    _, _, (ref, flow) = _states(name, batch)
+    cfg = _native.make_config(q.DecoderConfig(max_iterations=iters, early_termination=False), "fp32")
+    ref.decode(cfg)
+    want = ref.download()
+    want_res = ref.results()
+    for trial in range(4):  # dynamic tile schedule: every run interleaves differently
+        flow.decode(cfg)
+        got = flow.download()
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), trial
+        for a, b in zip(flow.results(), want_res):
+            assert np.array_equal(a, b), trial
+
+
+def test_flow_sweeps_with_syndrome(gpu):
+    """Whole sweeps through qcl_state_layers (the flow path of _sweep) with a random target."""
+    _, sched, (ref, flow) = _states("standin_v2_z100", 16, syndrome=True)
+    for st in (ref, flow):
+        st.reset(30.0)
+        for _ in range(5):
+            st.layers(0, len(sched.layers), 30.0, 1e-10)
+    a, b = ref.download(), flow.download()
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("snr", [0.161, 0.2])
+def test_flow_early_termination_matches(gpu, snr):
+    """ET decodes (one flow launch per sweep): words, flags and iteration counts identical."""
+    import paper_2004_09084_b200 as q
+
+    base, sched, index = load_code("standin_v2_z100")
+    n, m = base.n_cols * base.z, base.n_rows * base.z
+    llr = channel_llrs(n, snr, 0, 0, 48)
+    cfg = q.DecoderConfig(max_iterations=50, early_termination=True)
+    res = [q.LayeredDecoder(index, sched, cfg, engine=e).decode_batch_arrays(llr, np.zeros((48, m), np.uint8))
+           for e in (0, 4)]
+    for a, b in zip(*res):
+        assert np.array_equal(a, b)
+
+
+def test_flow_fresh_states_first_launch(gpu):
+    """A new decoder's first decode (table uploads immediately followed by the launch)."""
+    import paper_2004_09084_b200 as q
+
+    base, sched, index = load_code("standin_v2_z100")
+    n, m = base.n_cols * base.z, base.n_rows * base.z
+    llr = channel_llrs(n, 0.161, 0, 0, 64)
+    cfg = q.DecoderConfig(max_iterations=12, early_termination=False)
+    want = q.LayeredDecoder(index, sched, cfg, engine=0).decode_batch_arrays(llr, np.zeros((64, m), np.uint8))
+    for _ in range(3):
+        got = q.LayeredDecoder(index, sched, cfg, engine=4).decode_batch_arrays(llr, np.zeros((64, m), np.uint8))
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)

@@ -115,6 +115,10 @@ int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms);
 int qcl_state_results(qcl_state *st, uint8_t *words, uint8_t *converged, int64_t *iterations);
 /* The transmitted words of the last synthetic encode-mode fill, (B, n). */
 int qcl_state_truths(qcl_state *st, uint8_t *words);
+/* Campaign frame errors (reference bench.py:236-237): mismatch[b] = 1 when the decoded
+ * word of frame b (after qcl_state_decode) differs from its transmitted word -- the
+ * encode-mode truths of the last synthetic fill, else the all-zero word.  (B) bytes. */
+int qcl_state_frame_errors(qcl_state *st, uint8_t *mismatch);
 /* Copy the state's device LLR buffer back as float64 (B, n) (tests of the generator). */
 int qcl_state_get_llr(qcl_state *st, double *llr);
 /* Device-time breakdown of the last qcl_state_decode: number of layer-kernel launches and

@@ -63,6 +63,7 @@ _SIGNATURES = {
     "qcl_state_get_llr": ([_vp, _vp], ctypes.c_int),
     "qcl_state_kernel_stats": ([_vp, _vp, _vp, _vp], ctypes.c_int),
     "qcl_state_set_engine": ([_vp, _i32], ctypes.c_int),
+    "qcl_state_frame_errors": ([_vp, _vp], ctypes.c_int),
     "qcl_phi": ([_vp, _i64, _dbl, _dbl, _i32, _i32, _vp], ctypes.c_int),
     "qcl_state_set_syndrome_hint": ([_vp, _vp, _i32], ctypes.c_int),
     "qcl_state_decode_async": ([_vp, _vp], ctypes.c_int),
@@ -243,6 +244,12 @@ class State:
         w = np.empty((self.batch, self.plan.n), np.uint8)
         call("qcl_state_truths", self.handle, ptr(w))
         return w
+
+    def frame_errors(self):
+        """Per frame: decoded word differs from the transmitted one (qcl_state_frame_errors)."""
+        out = np.empty(self.batch, np.uint8)
+        call("qcl_state_frame_errors", self.handle, ptr(out))
+        return out.astype(bool)
 
     def get_llr(self):
         out = np.empty((self.batch, self.plan.n), np.float64)

@@ -97,6 +97,7 @@ struct qcl_state {
     int64_t *iters = nullptr;
     int *n_active = nullptr, *h_n_active = nullptr;  // device / pinned host
     uint8_t *truths = nullptr;
+    bool truths_valid = false;  // the last synthetic fill was encode mode (else all-zero words)
     void *staging = nullptr;
     size_t staging_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_done = nullptr;
@@ -977,6 +978,7 @@ int qcl_state_set_llr_synthetic(qcl_state *st, uint64_t seed, int64_t snr_idx, i
                                                                    (uint32_t)snr_idx, first_frame, sigma, sigma2,
                                                                    encode_mode, (double *)st->llr, tr);
     CK(cudaGetLastError());
+    st->truths_valid = encode_mode != 0;
     if (encode_mode) {
         SlotRange r = slot_range(st, 0, p->S, 1);
         dim3 g2((unsigned)((int64_t)st->G * p->S * r.bps));
@@ -994,12 +996,27 @@ int qcl_state_set_llr_synthetic(qcl_state *st, uint64_t seed, int64_t snr_idx, i
 int qcl_state_truths(qcl_state *st, uint8_t *words) {
     if (!st || !words) return fail(QCL_EVALUE, "NULL argument");
     CK(cudaSetDevice(st->plan->device));
-    if (!st->truths) {
+    if (!st->truths || !st->truths_valid) {
         CK(cudaStreamSynchronize(st->stream));
         memset(words, 0, (size_t)st->B * st->plan->n);
         return QCL_OK;
     }
     CK(cudaMemcpyAsync(words, st->truths, (size_t)st->B * st->plan->n, cudaMemcpyDeviceToHost, st->stream));
+    CK(cudaStreamSynchronize(st->stream));
+    return QCL_OK;
+}
+
+int qcl_state_frame_errors(qcl_state *st, uint8_t *mismatch) {
+    if (!st || !mismatch) return fail(QCL_EVALUE, "NULL argument");
+    const qcl_plan *p = st->plan;
+    CK(cudaSetDevice(p->device));
+    CK(cudaMemsetAsync(st->take, 0, st->B, st->stream));  // reused as the per-frame flag buffer
+    const int64_t units = (p->n % 16 == 0) ? p->n / 16 : p->n;
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(units, kBlock), 64));
+    frame_mismatch_kernel<<<dim3(gx, (unsigned)st->B), kBlock, 0, st->stream>>>(
+        st->words, st->truths_valid ? st->truths : nullptr, p->n, st->take);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(mismatch, st->take, st->B, cudaMemcpyDeviceToHost, st->stream));
     CK(cudaStreamSynchronize(st->stream));
     return QCL_OK;
 }

@@ -1,0 +1,174 @@
+"""Device campaigns (paper_2004_09084_b200.campaign) against the reference's own
+campaign reports (tests/golden/campaign_*.json, made by make_campaign_golden.py from
+the unmodified reference ``qcldpc.bench.run_campaign``).
+
+* host channel (bit-identical PCG64 frames), FP64 parity path: FER and average
+  iterations EXACTLY equal to the reference's;
+* host channel, FP32 path, and device (Philox) channel: FER inside the reference's
+  confidence interval, the acceptance-test form 1.96 * sqrt(p1 q1 / N + p2 q2 / N)
+  (tests/test_acceptance.py:194,236), with one frame of slack for p = 0 or 1.
+CPU-only tests cover validation and the CSV/JSON report schema.
+"""
+
+import csv
+import json
+import math
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT
+
+CASES = ["campaign_demo4x8z32_et50", "campaign_demo4x8z100_noet10", "campaign_demo4x8z32_encode"]
+
+
+def golden(name):
+    return json.loads((GOLDEN / f"{name}.json").read_text())
+
+
+def config_of(g, **over):
+    from paper_2004_09084_b200.campaign import CampaignConfig
+
+    c = g["metadata"]["campaign"]
+    kw = dict(
+        matrix_path=str(ROOT / "codes" / g["metadata"]["matrix"]["path"]),
+        snr_list=[x["snr"] for x in g["cells"]],
+        max_iterations=g["metadata"]["decoder"]["max_iterations"],
+        early_termination=g["metadata"]["decoder"]["early_termination"],
+        batch_size=c["batch_size"],
+        min_trials=c["min_trials"],
+        seed=c["seed"],
+        encode_mode=c["encode_mode"],
+    )
+    kw.update(over)
+    return CampaignConfig(**kw)
+
+
+def within_ci(p1, p2, n):
+    band = 1.96 * math.sqrt(p1 * (1 - p1) / n + p2 * (1 - p2) / n) + 1.0 / n
+    return abs(p1 - p2) <= band
+
+
+# ------------------------------------------------------------------------ CPU tests
+
+
+def test_config_validation_messages():
+    from paper_2004_09084_b200.campaign import CampaignConfig
+
+    path = str(ROOT / "codes" / "demo_4x8_z32.txt")
+    for kw, msg in [
+        (dict(snr_list=()), "snr_list must not be empty"),
+        (dict(snr_list=(1.0, -1.0)), "every snr must be positive"),
+        (dict(snr_list=(1.0,), batch_size=0), "batch_size must be at least 1"),
+        (dict(snr_list=(1.0,), batch_size=64, min_trials=8), "min_trials must be at least batch_size"),
+        (dict(snr_list=(1.0,), max_iterations=0), "max_iterations must be at least 1"),
+        (dict(snr_list=(1.0,), workers=0), "workers must be at least 1"),
+        (dict(snr_list=(1.0,), lane_budget=0), "lane_budget must be positive"),
+        (dict(snr_list=(1.0,), precision="fp16"), "precision must be one of"),
+        (dict(snr_list=(1.0,), channel="wire"), "channel must be one of"),
+    ]:
+        with pytest.raises(ValueError, match=msg):
+            CampaignConfig(matrix_path=path, **kw)
+    cfg = CampaignConfig(matrix_path=path, snr_list=[1, 2], batch_size=48, min_trials=100)
+    assert cfg.snr_list == (1.0, 2.0) and cfg.frames_per_point == 144
+
+
+def test_report_schema_csv_and_json(tmp_path):
+    from paper_2004_09084_b200.campaign import (
+        CSV_COLUMNS,
+        SCHEMA_VERSION,
+        CampaignCell,
+        CampaignReport,
+        ScheduleComparison,
+        emit_report,
+        report_to_dict,
+    )
+
+    cell = CampaignCell(1.0, 0.5, 7.5, 1e-3, 12.0, 0.9, 96, 0.01)
+    rep = CampaignReport(cells=(cell,), metadata={"schema_version": SCHEMA_VERSION})
+    d = report_to_dict(rep)
+    assert d["schema_version"] == 1 and d["cells"][0]["fer"] == 0.5
+    assert tuple(d["cells"][0]) == CSV_COLUMNS
+    p = emit_report(rep, "csv", tmp_path / "r.csv")
+    rows = list(csv.reader(p.open()))
+    assert tuple(rows[0]) == CSV_COLUMNS and float(rows[1][1]) == 0.5
+    cmp = ScheduleComparison(single=rep, merged=rep, single_layer_count=4, merged_layer_count=2)
+    p = emit_report(cmp, "csv", tmp_path / "c.csv")
+    rows = list(csv.reader(p.open()))
+    assert rows[0][0] == "schedule" and [r[0] for r in rows[1:]] == ["single", "merged"]
+    p = emit_report(cmp, "json", tmp_path / "c.json")
+    assert json.loads(p.read_text())["merged_layer_count"] == 2
+    with pytest.raises(ValueError, match="unknown report format"):
+        emit_report(rep, "xml", tmp_path / "r.xml")
+
+
+def test_golden_reports_have_reference_schema():
+    from paper_2004_09084_b200.campaign import CSV_COLUMNS, METRIC_DEFINITIONS
+
+    for name in CASES:
+        g = golden(name)
+        assert g["schema_version"] == 1
+        assert g["metadata"]["definitions"] == METRIC_DEFINITIONS
+        for cell in g["cells"]:
+            assert tuple(cell) == CSV_COLUMNS
+
+
+# ------------------------------------------------------------------------ GPU tests
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_host_channel_fp64_matches_reference_exactly(gpu, name):
+    from paper_2004_09084_b200.campaign import run_campaign
+
+    g = golden(name)
+    rep = run_campaign(config_of(g, precision="fp64"))
+    for got, want in zip(rep.cells, g["cells"]):
+        assert got.fer == want["fer"] and got.avg_iterations == want["avg_iterations"], (got, want)
+        assert got.beta == pytest.approx(want["beta"]) and got.total_expanded_edges == want["total_expanded_edges"]
+        assert got.utilization == pytest.approx(want["utilization"])
+        assert got.throughput_mbits_per_s > 0 and got.latency_per_iteration_s > 0
+    for key in ("matrix", "schedule", "decoder", "campaign", "definitions"):
+        want = dict(g["metadata"][key])
+        have = dict(rep.metadata[key])
+        if key == "matrix":
+            want.pop("path"), have.pop("path")
+        assert have == want, key
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("channel", ["host", "device"])
+def test_fp32_and_device_channel_within_reference_ci(gpu, name, channel):
+    from paper_2004_09084_b200.campaign import run_campaign
+
+    g = golden(name)
+    cfg = config_of(g, precision="fp32", channel=channel)
+    rep = run_campaign(cfg)
+    n = cfg.frames_per_point
+    for got, want in zip(rep.cells, g["cells"]):
+        assert within_ci(got.fer, want["fer"], n), (channel, got.snr, got.fer, want["fer"])
+
+
+@pytest.mark.gpu
+def test_device_channel_is_deterministic_and_shard_invariant(gpu):
+    """Same seed -> same FER/iterations, whatever the batch size (frames keyed by index)."""
+    from paper_2004_09084_b200.campaign import run_campaign
+
+    g = golden("campaign_demo4x8z32_et50")
+    a = run_campaign(config_of(g, channel="device", batch_size=64, min_trials=512))
+    b = run_campaign(config_of(g, channel="device", batch_size=128, min_trials=512))
+    for x, y in zip(a.cells, b.cells):
+        assert x.fer == y.fer and x.avg_iterations == y.avg_iterations
+
+
+@pytest.mark.gpu
+def test_compare_schedules_on_device(gpu, tmp_path):
+    from paper_2004_09084_b200.campaign import CampaignConfig, compare_schedules, emit_report
+
+    cfg = CampaignConfig(matrix_path=str(ROOT / "codes" / "demo_6x12_z16.txt"), snr_list=(2.0,),
+                         max_iterations=20, early_termination=True, batch_size=64, min_trials=128,
+                         channel="device")
+    cmp = compare_schedules(cfg)
+    assert cmp.single_layer_count == 6 and cmp.merged_layer_count < 6
+    assert emit_report(cmp, "csv", tmp_path / "cmp.csv").exists()

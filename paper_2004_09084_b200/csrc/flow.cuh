@@ -85,6 +85,7 @@ struct FlowArgs {
     int32_t stages;
     int32_t clip_r;
     const int *n_active;  // early termination: skip the launch once every frame converged
+    const uint8_t *gactive;  // early termination: lane groups with an active frame (others skipped)
     unsigned long long *stats;  // optional instrumentation (QCL_FLOW_STATS)
     double clip, eps;
     double mag_max;             // FP32 bound on |r| (LayerArgs::mag_max)
@@ -408,6 +409,13 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
                 const int KT = kFlowConsumers * 32 * flow_class_V(h.cls) / W;
                 h.k0 = e.y * KT;
                 h.kt = min(KT, a.z - h.k0);
+                if (a.gactive && !a.gactive[h.g]) {
+                    // every frame of this lane group has converged: its outputs are frozen,
+                    // so the tile is not updated -- only released for the group's later tiles
+                    __syncwarp();
+                    if (lane == 0) st_release(a.flags + (size_t)h.g * a.nkb_total + st.y + e.y, h.t + 1);
+                    goto next_item;
+                }
                 // wait for the previous writers of every column of this tile
                 int polls = 0;
                 const int *fg = a.flags + (size_t)h.g * a.nkb_total;
@@ -444,6 +452,9 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
                 q = 0;
                 ph ^= 1;
             }
+            continue;
+        next_item:
+            it--;  // nothing was queued: this queue slot is still free
         }
         if (prof && lane == 0) {
             for (int k = 0; k < 4; k++) atomicAdd(a.stats + 3 + k, (unsigned long long)acc[k]);

@@ -429,57 +429,110 @@ __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
 // ---- hard decisions and syndrome check on packed sign words ------------------------
 // signs[g][v]: bit w = (L[g][v][w] < 0) -- one uint32 per variable carries the hard
 // decisions of all W lanes (decoder.py:264-266; -0.0 decides to 0 like `< 0`).
+// Lane groups whose frames have all converged (early termination) are skipped when
+// gact != nullptr: their outputs were frozen at convergence, so nothing observable
+// depends on their later state.
+// signs[v][g]: bit w = (L[g][v][w] < 0), i.e. all lane groups of a variable side by side,
+// so one syndrome-check thread reads every group's sign word of a variable in one go.
 template <typename T>
-__global__ void __launch_bounds__(kBlock) sign_pack_kernel(const T *L, int64_t total, int lw, uint32_t *signs) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over G * n * W, lane fastest
-    const bool neg = i < total && __ldcg(L + i) < (T)0;
-    const uint32_t bits = __ballot_sync(0xffffffffu, neg);
-    const int W = 1 << lw, lane = threadIdx.x & 31;
-    if (i < total && (lane & (W - 1)) == 0) {
-        const uint32_t mask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
-        signs[i >> lw] = (bits >> lane) & mask;
+__global__ void __launch_bounds__(kBlock) sign_pack_kernel(const T *L, int64_t Gn, int lw, uint32_t *signs, int64_t n,
+                                                           const uint8_t *gact) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over G * n: one variable of one group
+    if (i >= Gn) return;
+    const int64_t g = i / n, v = i - g * n;
+    if (gact && !gact[g]) return;
+    const int W = 1 << lw;
+    const T *p = L + (i << lw);
+    uint32_t m = 0;
+    if (sizeof(T) == 4 && (W & 3) == 0) {  // W lanes = W/4 coalesced 16-byte loads
+        for (int w = 0; w < W; w += 4) {
+            const float4 x = __ldcg(reinterpret_cast<const float4 *>(p + w));
+            m |= ((uint32_t)(x.x < 0.0f) | ((uint32_t)(x.y < 0.0f) << 1) | ((uint32_t)(x.z < 0.0f) << 2) |
+                  ((uint32_t)(x.w < 0.0f) << 3)) << w;
+        }
+    } else {
+        for (int w = 0; w < W; w++) m |= (uint32_t)(__ldcg(p + w) < (T)0) << w;
     }
+    signs[v * (Gn / n) + g] = m;
+}
+
+// gact[g] = some frame of lane group g is still active (early termination).
+__global__ void group_active_kernel(int64_t Bp, int lw, const uint8_t *active, uint8_t *gact) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((g << lw) >= Bp) return;
+    uint8_t any = 0;
+    for (int w = 0; w < (1 << lw); w++) any |= active[(g << lw) + w];
+    gact[g] = any;
 }
 
 // Syndrome bytes (lanes layout) -> one uint32 of W lane bits per check.
-__global__ void syn_pack_kernel(const uint8_t *syn, int64_t words, int lw, uint32_t *packed) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+// Syndrome bytes (lanes layout u8[G][S][z][W]) -> packed[(s*z + k)*G + g], W lane bits.
+__global__ void syn_pack_kernel(const uint8_t *syn, int64_t words, int lw, int64_t Sz, uint32_t *packed) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over G * S * z, (g, check)
     if (i >= words) return;
     const int W = 1 << lw;
+    const int64_t G = words / Sz, g = i / Sz, c = i - g * Sz;
     uint32_t v = 0;
     for (int w = 0; w < W; w++) v |= (uint32_t)(syn[(i << lw) + w] & 1) << w;
-    packed[i] = v;
+    packed[c * G + g] = v;
 }
 
-// syndrome_satisfied (decoder.py:268-273) for all lanes at once: per check, XOR of the
-// packed sign words of its d variables (^ packed target syndrome); any set bit marks
-// that lane's codeword unsatisfied.  Lanes of a warp OR-reduce before one atomic.
+// syndrome_satisfied (decoder.py:268-273) for all lanes at once: one thread per check
+// (s, k) covers every lane group: XOR of the d variables' sign words (^ packed target
+// syndrome); a set bit marks that lane's codeword unsatisfied.  Lanes OR-reduce per
+// group before one atomic.  Groups in chunks of 8 (two 16-byte loads per variable).
 __global__ void __launch_bounds__(kBlock) check_packed_kernel(const SlotInfo *slots, const EdgeInfo *edges,
                                                               int64_t n, int S, int z, int G,
                                                               const uint32_t *signs, const uint32_t *synpack,
-                                                              uint32_t *unsat_mask) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over G * S * z
-    const int64_t total = (int64_t)G * S * z;
-    int g = -1;
-    uint32_t p = 0;
-    if (i < total) {
-        const int k = (int)(i % z);
-        const int64_t rest = i / z;
-        const int s = (int)(rest % S);
-        g = (int)(rest / S);
-        const SlotInfo si = slots[s];
-        const uint32_t *sg = signs + (int64_t)g * n;
-        p = synpack ? synpack[i] : 0u;
-        for (int j = 0; j < si.degree; j++) {
-            const EdgeInfo e = edges[si.edge_off + j];
-            int pos = k + e.shift;
-            pos -= (pos >= z) ? z : 0;
-            p ^= __ldg(sg + e.var_base + pos);
+                                                              uint32_t *unsat_mask, const uint8_t *gact) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;  // over S * z checks (< 2^31)
+    const uint32_t total = (uint32_t)S * (uint32_t)z;
+    const bool live = i < total;
+    const uint32_t s = live ? i / (uint32_t)z : 0, k = live ? i - s * (uint32_t)z : 0;
+    const SlotInfo si = live ? slots[s] : SlotInfo{0, 0, 0, 0};
+    const bool vec = (G & 3) == 0;
+    for (int g0 = 0; g0 < G; g0 += 8) {
+        bool any_active = true;
+        if (gact) {
+            any_active = false;
+            for (int c = 0; c < 8 && g0 + c < G; c++) any_active |= gact[g0 + c] != 0;
         }
+        if (!any_active) continue;  // warp-uniform: every frame of these groups converged
+        uint32_t p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const int cnt = min(8, G - g0);
+        if (live) {
+            if (synpack)
+                for (int c = 0; c < cnt; c++) p[c] = synpack[(int64_t)i * G + g0 + c];
+            for (int j = 0; j < si.degree; j++) {
+                const EdgeInfo e = edges[si.edge_off + j];
+                int pos = (int)k + e.shift;
+                pos -= (pos >= z) ? z : 0;
+                const uint32_t *row = signs + (int64_t)(e.var_base + pos) * G + g0;
+                if (vec && cnt == 8) {
+                    const uint4 a = __ldg(reinterpret_cast<const uint4 *>(row));
+                    const uint4 b = __ldg(reinterpret_cast<const uint4 *>(row) + 1);
+                    p[0] ^= a.x; p[1] ^= a.y; p[2] ^= a.z; p[3] ^= a.w;
+                    p[4] ^= b.x; p[5] ^= b.y; p[6] ^= b.z; p[7] ^= b.w;
+                } else {
+                    for (int c = 0; c < cnt; c++) p[c] ^= __ldg(row + c);
+                }
+            }
+        }
+        // warp OR-reduce, then block OR in shared memory: one global atomic per group and
+        // block (same-address global atomics from every warp serialise in L2)
+        __shared__ uint32_t s_acc[8];
+        if (threadIdx.x < 8) s_acc[threadIdx.x] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            const uint32_t any = __reduce_or_sync(0xffffffffu, p[c]);
+            if (any && (threadIdx.x & 31) == 0) atomicOr(&s_acc[c], any);
+        }
+        __syncthreads();
+        if (threadIdx.x < 8 && g0 + (int)threadIdx.x < G && s_acc[threadIdx.x])
+            atomicOr(unsat_mask + g0 + threadIdx.x, s_acc[threadIdx.x]);
+        __syncthreads();
     }
-    const uint32_t same = __match_any_sync(0xffffffffu, g);
-    const uint32_t any = __reduce_or_sync(same, p);
-    if (g >= 0 && any && (threadIdx.x & 31) == __ffs(same) - 1) atomicOr(unsat_mask + g, any);
 }
 
 // Words (B, n) from packed signs for the codewords with take[b] (all if take == nullptr).
@@ -487,12 +540,22 @@ __global__ void __launch_bounds__(kBlock) check_packed_kernel(const SlotInfo *sl
 // common early-termination iteration) costs n/256 blocks reading B flags.
 __global__ void __launch_bounds__(kBlock) words_from_signs_kernel(const uint32_t *signs, int64_t n, int lw,
                                                                   int64_t B, const uint8_t *take, uint8_t *words) {
+    const int64_t G = (B + (1 << lw) - 1) >> lw;
+    if (take) {  // most early-termination sweeps take no frame: the whole block exits
+        __shared__ int s_any;
+        if (threadIdx.x == 0) s_any = 0;
+        __syncthreads();
+        for (int64_t b = threadIdx.x; b < B; b += blockDim.x)
+            if (take[b]) s_any = 1;
+        __syncthreads();
+        if (!s_any) return;
+    }
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     const int Wm = (1 << lw) - 1;
     for (int64_t b = 0; b < B; b++) {
         if (take && !take[b]) continue;
-        words[b * n + v] = (uint8_t)((__ldg(signs + (b >> lw) * n + v) >> (b & Wm)) & 1u);
+        words[b * n + v] = (uint8_t)((__ldg(signs + v * G + (b >> lw)) >> (b & Wm)) & 1u);
     }
 }
 

@@ -91,6 +91,7 @@ struct qcl_state {
     uint8_t *syn = nullptr;  // lanes layout, valid if has_syn
     bool has_syn = false;
     uint8_t *words = nullptr, *conv = nullptr, *active = nullptr, *take = nullptr;
+    uint8_t *gactive = nullptr;  // [G] lane groups with an active frame (early termination)
     uint32_t *unsat = nullptr;    // [G] lane bit masks of unsatisfied codewords
     uint32_t *signs = nullptr;    // [G][n] packed hard decisions
     uint32_t *synpack = nullptr;  // [G][S][z] packed target syndrome (valid if has_syn)
@@ -502,6 +503,7 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.stages = st->f_stages;
     a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));  // |r| <= Phi(eps)
     a.n_active = et ? st->n_active : nullptr;
+    a.gactive = et ? st->gactive : nullptr;
     a.stats = st->fstats;
     a.clip = clip;
     a.eps = eps;
@@ -520,31 +522,40 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
 }
 
 // Hard decisions of every lane packed into sign words (decoder.py:264-266).
-static int enqueue_signs(qcl_state *st) {
+static int enqueue_signs(qcl_state *st, const uint8_t *gact = nullptr) {
     const qcl_plan *p = st->plan;
-    const int64_t total = st->Bp * p->n;
-    const unsigned grid = (unsigned)cdiv(total, kBlock);
+    const int64_t Gn = (int64_t)st->G * p->n;
+    const unsigned grid = (unsigned)cdiv(Gn, kBlock);
     if (st->prec == QCL_PREC_FP32)
-        sign_pack_kernel<float><<<grid, kBlock, 0, st->stream>>>((const float *)st->L, total, st->lw, st->signs);
+        sign_pack_kernel<float><<<grid, kBlock, 0, st->stream>>>((const float *)st->L, Gn, st->lw, st->signs, p->n,
+                                                                  gact);
     else
-        sign_pack_kernel<double><<<grid, kBlock, 0, st->stream>>>((const double *)st->L, total, st->lw, st->signs);
+        sign_pack_kernel<double><<<grid, kBlock, 0, st->stream>>>((const double *)st->L, Gn, st->lw, st->signs,
+                                                                   p->n, gact);
     st->launches_all++;
     CK(cudaGetLastError());
     return QCL_OK;
 }
 
-// syndrome_satisfied for every codeword (decoder.py:268-273) -> st->unsat lane masks.
-static int enqueue_check(qcl_state *st) {
+// syndrome_satisfied for every codeword (decoder.py:268-273) -> st->unsat lane masks;
+// with gact, lane groups whose frames have all converged are skipped.
+static int enqueue_check(qcl_state *st, const uint8_t *gact = nullptr) {
     const qcl_plan *p = st->plan;
-    int rc = enqueue_signs(st);
+    int rc = enqueue_signs(st, gact);
     if (rc) return rc;
     CK(cudaMemsetAsync(st->unsat, 0, sizeof(uint32_t) * st->G, st->stream));
-    const int64_t total = (int64_t)st->G * p->S * p->z;
+    const int64_t total = (int64_t)p->S * p->z;
     check_packed_kernel<<<(unsigned)cdiv(total, kBlock), kBlock, 0, st->stream>>>(
-        p->slots, p->edges, p->n, p->S, p->z, st->G, st->signs, st->has_syn ? st->synpack : nullptr, st->unsat);
+        p->slots, p->edges, p->n, p->S, p->z, st->G, st->signs, st->has_syn ? st->synpack : nullptr, st->unsat, gact);
     st->launches_all++;
     CK(cudaGetLastError());
     return QCL_OK;
+}
+
+static void enqueue_group_active(qcl_state *st) {
+    group_active_kernel<<<(unsigned)cdiv(st->G, kBlock), kBlock, 0, st->stream>>>(st->Bp, st->lw, st->active,
+                                                                                    st->gactive);
+    st->launches_all++;
 }
 
 // Words (B, n) for codewords with take[b] from the packed signs of the last check.
@@ -560,7 +571,8 @@ static int enqueue_words(qcl_state *st, const uint8_t *take) {
 static int enqueue_syn_pack(qcl_state *st) {
     const qcl_plan *p = st->plan;
     const int64_t words = (int64_t)st->G * p->S * p->z;
-    syn_pack_kernel<<<(unsigned)cdiv(words, kBlock), kBlock, 0, st->stream>>>(st->syn, words, st->lw, st->synpack);
+    syn_pack_kernel<<<(unsigned)cdiv(words, kBlock), kBlock, 0, st->stream>>>(st->syn, words, st->lw,
+                                                                               (int64_t)p->S * p->z, st->synpack);
     CK(cudaGetLastError());
     return QCL_OK;
 }
@@ -826,6 +838,10 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
     st->W = 1 << st->lw;
     st->G = (int)cdiv(batch, st->W);
     st->Bp = (int64_t)st->G * st->W;
+    if ((int64_t)st->G * p->S * p->z >= (1LL << 31) || st->Bp * p->n >= (1LL << 40)) {
+        delete st;
+        return fail(QCL_EUNSUP, "batch %lld too large for one state (split it across states)", (long long)batch);
+    }
     const size_t nl = (size_t)st->Bp * p->n, ne = (size_t)st->Bp * p->E * p->z, nm = (size_t)st->Bp * p->m;
     cudaError_t e = cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking);
     for (int i = 0; i < kSideStreams && e == cudaSuccess; i++) {
@@ -846,6 +862,7 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
     al((void **)&st->signs, sizeof(uint32_t) * st->G * p->n);
     al((void **)&st->synpack, sizeof(uint32_t) * st->G * p->S * p->z);
     al((void **)&st->active, st->Bp);
+    al((void **)&st->gactive, st->G);
     al((void **)&st->take, st->Bp);
     al((void **)&st->iters, st->Bp * sizeof(int64_t));
     al((void **)&st->n_active, sizeof(int));
@@ -884,7 +901,7 @@ int qcl_state_destroy(qcl_state *st) {
     if (st->sweep_exec) cudaGraphExecDestroy(st->sweep_exec);
     if (st->decode_exec) cudaGraphExecDestroy(st->decode_exec);
     for (void *ptr : {st->llr, st->L, st->R, (void *)st->syn, (void *)st->words, (void *)st->conv,
-                      (void *)st->unsat, (void *)st->signs, (void *)st->synpack, (void *)st->active,
+                      (void *)st->unsat, (void *)st->signs, (void *)st->synpack, (void *)st->active, (void *)st->gactive,
                       (void *)st->take, (void *)st->iters,
                       (void *)st->n_active, (void *)st->truths, st->staging, (void *)st->fslot_tab,
                       (void *)st->fitems, (void *)st->fflags, (void *)st->fcounters, (void *)st->fstats})
@@ -1214,6 +1231,7 @@ static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
     decode_init_kernel<<<(unsigned)cdiv(st->Bp, kBlock), kBlock, 0, st->stream>>>(
         st->B, st->Bp, cfg->max_iterations, st->active, st->conv, st->iters, st->n_active);
     st->launches_all++;
+    enqueue_group_active(st);
     if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
     st->g_et = et;
     const bool flow = st->flow_decode;
@@ -1235,13 +1253,14 @@ static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
         }
         st->launches_all += st->launches_layer - before;
         if (!et) continue;
-        if ((rc = enqueue_check(st))) return rc;
+        if ((rc = enqueue_check(st, st->gactive))) return rc;
         et_update_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, t, st->unsat, st->lw, st->active, st->take, st->conv,
                                                         st->iters, st->n_active);
         st->launches_all++;
         if ((rc = enqueue_words(st, st->take))) return rc;
+        enqueue_group_active(st);
     }
-    if ((rc = enqueue_check(st))) return rc;
+    if ((rc = enqueue_check(st, st->gactive))) return rc;
     finalize_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, st->unsat, st->lw, st->active, st->take, st->conv);
     st->launches_all++;
     return enqueue_words(st, st->take);
@@ -1303,6 +1322,7 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     decode_init_kernel<<<(unsigned)cdiv(st->Bp, kBlock), kBlock, 0, st->stream>>>(
         st->B, st->Bp, cfg->max_iterations, st->active, st->conv, st->iters, st->n_active);
     st->launches_all++;
+    enqueue_group_active(st);
     if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
     const unsigned gb = (unsigned)cdiv(st->B, kBlock);
     const bool flow = st->flow_decode;
@@ -1327,11 +1347,12 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
             return rc;
         }
         if (!et) continue;
-        if ((rc = enqueue_check(st))) return rc;
+        if ((rc = enqueue_check(st, st->gactive))) return rc;
         et_update_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, t, st->unsat, st->lw, st->active, st->take, st->conv,
                                                         st->iters, st->n_active);
         st->launches_all++;
         if ((rc = enqueue_words(st, st->take))) return rc;
+        enqueue_group_active(st);
         if (!sync) continue;
         CK(cudaMemcpyAsync(st->h_flag + (t & 1), st->n_active, sizeof(int), cudaMemcpyDeviceToHost, st->stream));
         CK(cudaEventRecord(st->ev_flag[t & 1], st->stream));
@@ -1340,7 +1361,7 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
             if (st->h_flag[(t - 1) & 1] == 0) break;
         }
     }
-    if ((rc = enqueue_check(st))) return rc;
+    if ((rc = enqueue_check(st, st->gactive))) return rc;
     finalize_kernel<<<gb, kBlock, 0, st->stream>>>(st->B, st->unsat, st->lw, st->active, st->take, st->conv);
     st->launches_all++;
     if ((rc = enqueue_words(st, st->take))) return rc;

@@ -86,6 +86,7 @@ struct FlowArgs {
     int32_t clip_r;
     const int *n_active;  // early termination: skip the launch once every frame converged
     const uint8_t *gactive;  // early termination: lane groups with an active frame (others skipped)
+    int32_t defer_last;      // >= 0: degree-1 edges keep q in the L slot and no R until sweep defer_last
     unsigned long long *stats;  // optional instrumentation (QCL_FLOW_STATS)
     double clip, eps;
     double mag_max;             // FP32 bound on |r| (LayerArgs::mag_max)
@@ -136,6 +137,9 @@ __device__ __forceinline__ void flow_runs(const FlowArgs &a, const FlowHdr &h, c
         const uint32_t ex = etab[h.edge_off + j].x;
         const int col = ex & 0x7fff, shift = ex >> 16;
         const bool reused = (ex >> 15) & 1;
+        // degree-1 column under deferral (see flow_deferred): no R run moves, except the
+        // final store of the last sweep
+        const bool skip_r = !reused && a.defer_last >= 0 && (load || h.t != a.defer_last);
         int p0 = h.k0 + shift;
         p0 -= (p0 >= z) ? z : 0;
         const int len1 = min(h.kt, z - p0);
@@ -152,18 +156,34 @@ __device__ __forceinline__ void flow_runs(const FlowArgs &a, const FlowHdr &h, c
         if (load) {
             bulk_load(ls, lg1, b1, bar, pl);
             if (b2) bulk_load(ls + (size_t)len1 * W, lg2, b2, bar, pl);
-            bulk_load(rs, rg, br, bar, pol_stream);
+            if (!skip_r) bulk_load(rs, rg, br, bar, pol_stream);
         } else {
             bulk_store(lg1, ls, b1, pl);
             if (b2) bulk_store(lg2, ls + (size_t)len1 * W, b2, pl);
-            bulk_store(rg, rs, br, pol_stream);
+            if (!skip_r) bulk_store(rg, rs, br, pol_stream);
         }
     }
 }
 
+// Degree-1 deferral (bit-identical, fewer bytes).  A degree-1 column is touched by one
+// check only, so between sweeps the only use of its posterior L and message R is the next
+// sweep's q = clip(L - r) for that same edge.  Under deferral (the fused no-ET decode)
+// the consumer computes that q right away, q' = clip(clip(q + r) - r) -- the very FP32
+// operations the next sweep would do -- and leaves it in the L slot; no R moves.  The
+// last sweep (t == defer_last) writes the true L = clip(q + r) and R = r, so the final
+// state equals the undeferred one bit for bit.  Saves 8 of the 16 bytes per degree-1 edge
+// and sweep (23% of the edges of the rate-0.1 code, ~19% of its DRAM traffic).
+__device__ __forceinline__ uint32_t flow_deferred_mask(const FlowArgs &a, const FlowHdr &h, const uint2 *etab) {
+    if (a.defer_last < 0) return 0u;
+    uint32_t m = 0;
+    for (int j = 0; j < h.d; j++) m |= (((etab[h.edge_off + j].x >> 15) & 1u) ^ 1u) << j;
+    return m;
+}
+
 // One consumer thread: check (ci) of the tile for V lanes, in place in the stage.
 template <int V, int D, bool HAS_SYN>
-__device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct) {
+__device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
+                                             const uint2 *etab) {
     const int W = 1 << a.lw;
     const int KT = kFlowConsumers * 32 * V / W;
     const int KTW = KT * W;
@@ -176,6 +196,8 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
     using VT = typename Vec<float, V>::type;
     float q[D][V], ph[D][V];
     int par[V];
+    const uint32_t dmask = flow_deferred_mask(a, h, etab);
+    const bool last = h.t == a.defer_last;
     if (HAS_SYN) {
         const uint8_t *sp = a.syn + ((((int64_t)h.g * a.S + h.slot) * a.z + h.k0 + ci) << a.lw) + w0;
 #pragma unroll
@@ -189,9 +211,14 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
         if (j < h.d) {
             float lv[V], rv[V];
             *reinterpret_cast<VT *>(lv) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
-            *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+            if ((dmask >> j) & 1) {  // the L slot already holds q
 #pragma unroll
-            for (int v = 0; v < V; v++) q[j][v] = clampT(lv[v] - rv[v], clip);
+                for (int v = 0; v < V; v++) q[j][v] = lv[v];
+            } else {
+                *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+#pragma unroll
+                for (int v = 0; v < V; v++) q[j][v] = clampT(lv[v] - rv[v], clip);
+            }
         } else {
 #pragma unroll
             for (int v = 0; v < V; v++) q[j][v] = 0.0f;
@@ -209,6 +236,10 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
 #pragma unroll
     for (int j = 0; j < D; j++) {
         if (j < h.d) {
+            if (((dmask >> j) & 1) && !last) {  // next sweep's q for a deferred degree-1 edge
+#pragma unroll
+                for (int v = 0; v < V; v++) q[j][v] = clampT(q[j][v] - ph[j][v], clip);
+            }
             *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(ph[j]);
             *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(q[j]);
         }
@@ -221,7 +252,8 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
 // budget of two resident CTAs per SM holds without spills.  Same arithmetic, in the same
 // order, as check_update_f32.
 template <int V, int D, bool HAS_SYN>
-__device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHdr &h, float *stage, int ct) {
+__device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
+                                                 const uint2 *etab) {
     const int W = 1 << a.lw;
     const int KT = kFlowConsumers * 32 * V / W;
     const int KTW = KT * W;
@@ -234,6 +266,8 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
     using VT = typename Vec<float, V>::type;
     float q[D][V], t[D][V];
     int par[V];
+    const uint32_t dmask = flow_deferred_mask(a, h, etab);
+    const bool last = h.t == a.defer_last;
     if (HAS_SYN) {
         const uint8_t *sp = a.syn + ((((int64_t)h.g * a.S + h.slot) * a.z + h.k0 + ci) << a.lw) + w0;
 #pragma unroll
@@ -253,9 +287,10 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
             float lv[V], rv[V];
             *reinterpret_cast<VT *>(lv) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
             *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+            const bool dj = (dmask >> j) & 1;  // the L slot already holds q
 #pragma unroll
             for (int v = 0; v < V; v++) {
-                q[j][v] = clampT(lv[v] - rv[v], clip);
+                q[j][v] = dj ? lv[v] : clampT(lv[v] - rv[v], clip);
                 t[j][v] = sd_t(q[j][v]);
                 par[v] ^= (q[j][v] < 0.0f);
             }
@@ -301,6 +336,7 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
                 const float mag = sd_mag(S, Dv, mag_max);
                 rr[v] = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
                 ll[v] = clampT(q[j][v] + rr[v], clip);
+                if (((dmask >> j) & 1) && !last) ll[v] = clampT(ll[v] - rr[v], clip);  // deferred: next q
                 const float ns = fmaf(t[j][v], sd[v], ss[v]);
                 sd[v] = fmaf(t[j][v], ss[v], sd[v]);
                 ss[v] = ns;
@@ -489,9 +525,11 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
             } else {
                 fence_proxy_async_global();  // observed flags -> ordered before the bulk (async proxy) reads
                 const int KT = kFlowConsumers * 32 * flow_class_V(h.cls) / W;
+                // runs moved: d L runs, plus the R runs of edges not under degree-1 deferral
+                const uint32_t nr = (uint32_t)h.d - __popc(flow_deferred_mask(a, h, etab));
                 if (lane == 0) {
                     hdr[s] = h;
-                    mbar_arrive_expect_tx(&full[s], (uint32_t)(2 * h.d * h.kt * W * 4));
+                    mbar_arrive_expect_tx(&full[s], ((uint32_t)h.d + nr) * (uint32_t)(h.kt * W * 4));
                 }
                 __syncwarp();
                 flow_runs(a, h, etab, KT, flow_class_D(h.cls), stages + (size_t)s * kStageElems, &full[s], true,
@@ -555,11 +593,11 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
         } else {
             float *stage = stages + (size_t)s * kStageElems;
             if (h.cls == 0)
-                flow_consume<4, 4, HAS_SYN>(a, h, stage, ct);
+                flow_consume<4, 4, HAS_SYN>(a, h, stage, ct, etab);
             else if (h.cls == 1)
-                flow_consume_gen<2, 8, HAS_SYN>(a, h, stage, ct);
+                flow_consume_gen<2, 8, HAS_SYN>(a, h, stage, ct, etab);
             else
-                flow_consume_gen<1, 12, HAS_SYN>(a, h, stage, ct);
+                flow_consume_gen<1, 12, HAS_SYN>(a, h, stage, ct, etab);
             fence_proxy_async_smem();  // this thread's STS -> visible to the bulk-store engine
             __syncwarp();
             if (lane == 0) mbar_arrive(&done[s]);

@@ -470,6 +470,12 @@ static int ensure_flow(qcl_state *st, int counters) {
     return QCL_OK;
 }
 
+// Last sweep of a fused no-ET decode, or -1 with QCL_FLOW_DEFER=0 (degree-1 deferral off).
+static int flow_defer_last(int max_iterations) {
+    static int on = env_int("QCL_FLOW_DEFER", 1);
+    return on ? max_iterations - 1 : -1;
+}
+
 // Flags and claim counters back to zero: the start of a flow decode (sweep 0).
 static int enqueue_flow_reset(qcl_state *st, int counters) {
     int rc = ensure_flow(st, counters);
@@ -480,7 +486,8 @@ static int enqueue_flow_reset(qcl_state *st, int counters) {
 }
 
 // Sweeps [t0, t0 + T) in one persistent launch using claim counter `counter`.
-static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, int counter, bool et) {
+static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, int counter, bool et,
+                        int defer_last = -1) {
     const qcl_plan *p = st->plan;
     FlowArgs a;
     a.slot_tab = st->fslot_tab;
@@ -504,6 +511,7 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));  // |r| <= Phi(eps)
     a.n_active = et ? st->n_active : nullptr;
     a.gactive = et ? st->gactive : nullptr;
+    a.defer_last = defer_last;
     a.stats = st->fstats;
     a.clip = clip;
     a.eps = eps;
@@ -1237,8 +1245,9 @@ static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
     const bool flow = st->flow_decode;
     if (flow) {
         if ((rc = enqueue_flow_reset(st, et ? cfg->max_iterations : 1))) return rc;
-        if (!et) {  // every sweep in one persistent launch
-            if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, 0, cfg->max_iterations, 0, false)))
+        if (!et) {  // every sweep in one persistent launch, degree-1 edges deferred
+            if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, 0, cfg->max_iterations, 0, false,
+                                   flow_defer_last(cfg->max_iterations))))
                 return rc;
         }
     }
@@ -1337,7 +1346,9 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
                 CK(cudaEventCreate(&b));
                 CK(cudaEventRecord(a, st->stream));
             }
-            if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, t - 1, T, t - 1, et))) return rc;
+            if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, t - 1, T, t - 1, et,
+                                   et ? -1 : flow_defer_last(cfg->max_iterations))))
+                return rc;
             if (st->profiling) {
                 CK(cudaEventRecord(b, st->stream));
                 st->sweep_events.push_back({a, b});

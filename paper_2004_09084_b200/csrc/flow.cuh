@@ -41,6 +41,15 @@
 
 #include "pipeline.cuh"
 
+#ifndef QCL_FLOW_STAGE_KB
+#define QCL_FLOW_STAGE_KB 32
+#endif
+#ifndef QCL_FLOW_RELAXED_RELEASE
+#define QCL_FLOW_RELAXED_RELEASE 0
+#endif
+#ifndef QCL_FLOW_NOMATH
+#define QCL_FLOW_NOMATH 0
+#endif
 #ifndef QCL_FLOW_QUEUE
 #define QCL_FLOW_QUEUE 2
 #endif
@@ -50,12 +59,19 @@
 
 namespace qcl {
 
-constexpr int kFlowConsumers = 8;                  // consumer warps per CTA
-constexpr int kFlowStorers = 2;                    // storer warps per CTA
+#ifndef QCL_FLOW_WIDE
+#define QCL_FLOW_WIDE 0
+#endif
+// QCL_FLOW_WIDE = 0: two CTAs per SM, 8 consumer warps each; 1: one CTA per SM whose 16
+// consumer warps share every tile (half the service time per tile, so half the time a
+// claimed tile spends queued), with more storers and a deeper ring
+constexpr int kFlowConsumers = QCL_FLOW_WIDE ? 16 : 8;  // consumer warps per CTA
+constexpr int kFlowStorers = QCL_FLOW_WIDE ? 4 : 2;     // storer warps per CTA
+constexpr int kFlowCtasPerSm = QCL_FLOW_WIDE ? 1 : 2;
 constexpr int kFlowThreads = 32 * (kFlowConsumers + 2 + kFlowStorers);
 constexpr int kFlowQueue = QCL_FLOW_QUEUE;         // scheduler -> loader header queue depth
-constexpr int kFlowStageBytes = 32 * 1024;         // 2*D*KT*W*4 <= 32 KB for every class
-constexpr int kFlowMaxStages = 4;
+constexpr int kFlowStageBytes = QCL_FLOW_STAGE_KB * 1024;  // one ring stage (2*D*KT*W floats)
+constexpr int kFlowMaxStages = 6;
 constexpr int kFlowHeadBytes = 512;                // mbarriers + stage headers + header queue
 
 // Packed plan tables, copied into shared memory at kernel start (every producer/storer
@@ -92,8 +108,18 @@ struct FlowArgs {
     double mag_max;             // FP32 bound on |r| (LayerArgs::mag_max)
 };
 
-__host__ __device__ constexpr int flow_class_V(int cls) { return cls == 0 ? 4 : cls == 1 ? 2 : 1; }
 __host__ __device__ constexpr int flow_class_D(int cls) { return cls == 0 ? 4 : cls == 1 ? 8 : 12; }
+// lanes per consumer thread by degree class (the tile is KT checks x W lanes shared by all
+// consumer threads), and checks per tile: as many as the consumer threads cover, capped so
+// that 2*D*KT*W floats fit one ring stage
+__host__ __device__ constexpr int flow_class_V(int cls) {
+    return kFlowConsumers >= 16 ? (cls == 0 ? 2 : 1) : (cls == 0 ? 4 : cls == 1 ? 2 : 1);
+}
+__host__ __device__ constexpr int flow_KT(int cls, int W) {
+    return (kFlowConsumers * 32 * flow_class_V(cls) / W) < (kFlowStageBytes / (8 * flow_class_D(cls) * W))
+               ? (kFlowConsumers * 32 * flow_class_V(cls) / W)
+               : (kFlowStageBytes / (8 * flow_class_D(cls) * W));
+}
 __host__ __device__ constexpr size_t flow_smem_bytes(int S, int E, int stages) {
     return ((kFlowHeadBytes + 8 * (size_t)(S + E) + 127) / 128) * 128 + (size_t)stages * kFlowStageBytes;
 }
@@ -185,7 +211,7 @@ template <int V, int D, bool HAS_SYN>
 __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
                                              const uint2 *etab) {
     const int W = 1 << a.lw;
-    const int KT = kFlowConsumers * 32 * V / W;
+    const int KT = flow_KT(h.cls, W);
     const int KTW = KT * W;
     const int lanes_v = W / V;
     const int ci = ct / lanes_v;
@@ -224,6 +250,14 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
             for (int v = 0; v < V; v++) q[j][v] = 0.0f;
         }
     }
+#if QCL_FLOW_NOMATH  // timing experiment only: data movement without the check-node math
+    if (true) {
+#pragma unroll
+        for (int j = 0; j < D; j++)
+#pragma unroll
+            for (int v = 0; v < V; v++) ph[j][v] = 0.5f * q[j][v];
+    } else
+#endif
     if (D == 4 && h.d == 4) {
         uint32_t sb[V];
 #pragma unroll
@@ -255,7 +289,7 @@ template <int V, int D, bool HAS_SYN>
 __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
                                                  const uint2 *etab) {
     const int W = 1 << a.lw;
-    const int KT = kFlowConsumers * 32 * V / W;
+    const int KT = flow_KT(h.cls, W);
     const int KTW = KT * W;
     const int lanes_v = W / V;
     const int ci = ct / lanes_v;
@@ -355,7 +389,7 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
     }
 
 template <bool HAS_SYN, bool PROF>
-__global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
+__global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(FlowArgs a) {
     if (a.n_active && *(volatile const int *)a.n_active == 0) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);  // loader -> consumers (+tx)
@@ -442,7 +476,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
                 h.edge_off = st.x & 0xffff;
                 h.d = (st.x >> 16) & 0xff;
                 h.cls = st.x >> 24;
-                const int KT = kFlowConsumers * 32 * flow_class_V(h.cls) / W;
+                const int KT = flow_KT(h.cls, W);
                 h.k0 = e.y * KT;
                 h.kt = min(KT, a.z - h.k0);
                 if (a.gactive && !a.gactive[h.g]) {
@@ -460,7 +494,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
                     const int need = h.t + 1 - (int)((dy >> 15) & 1);
                     if (need <= 0) continue;
                     const uint2 pst = stab[dy & 0x7fff];
-                    const int KTp = kFlowConsumers * 32 * flow_class_V(pst.x >> 24) / W;
+                    const int KTp = flow_KT(pst.x >> 24, W);
                     const int *fl = fg + pst.y;
                     int a0 = h.k0 + (int)(dy >> 16);
                     a0 -= (a0 >= a.z) ? a.z : 0;
@@ -524,7 +558,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
                 if (++sentinels == kFlowStorers) break;
             } else {
                 fence_proxy_async_global();  // observed flags -> ordered before the bulk (async proxy) reads
-                const int KT = kFlowConsumers * 32 * flow_class_V(h.cls) / W;
+                const int KT = flow_KT(h.cls, W);
                 // runs moved: d L runs, plus the R runs of edges not under degree-1 deferral
                 const uint32_t nr = (uint32_t)h.d - __popc(flow_deferred_mask(a, h, etab));
                 if (lane == 0) {
@@ -557,7 +591,7 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
             if (sprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
             const FlowHdr h = hdr[s];
             if (h.kt < 0) break;
-            const int KT = kFlowConsumers * 32 * flow_class_V(h.cls) / W;
+            const int KT = flow_KT(h.cls, W);
             flow_runs(a, h, etab, KT, flow_class_D(h.cls), stages + (size_t)s * kStageElems, nullptr, false,
                       pol_keep, pol_stream);
             bulk_commit();
@@ -569,8 +603,16 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
             bulk_wait_all();  // this lane's writes are performed ...
             fence_proxy_async_global();
             __syncwarp();
-            if (lane == 0)  // ... before the tile is released to its dependents
+            if (lane == 0) {  // ... before the tile is released to its dependents
+#if QCL_FLOW_RELAXED_RELEASE  // timing experiment only: races (tools/flow_stress.py)
+                asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(a.flags + (size_t)h.g * a.nkb_total +
+                                                                        stab[h.slot].y + h.k0 / KT),
+                             "r"(h.t + 1)
+                             : "memory");
+#else
                 st_release(a.flags + (size_t)h.g * a.nkb_total + stab[h.slot].y + h.k0 / KT, h.t + 1);
+#endif
+            }
             if (sprof) acc[3] += clock64() - tc;
         }
         if (sprof && lane == 0)
@@ -593,11 +635,11 @@ __global__ void __launch_bounds__(kFlowThreads, 2) flow_kernel(FlowArgs a) {
         } else {
             float *stage = stages + (size_t)s * kStageElems;
             if (h.cls == 0)
-                flow_consume<4, 4, HAS_SYN>(a, h, stage, ct, etab);
+                flow_consume<flow_class_V(0), 4, HAS_SYN>(a, h, stage, ct, etab);
             else if (h.cls == 1)
-                flow_consume_gen<2, 8, HAS_SYN>(a, h, stage, ct, etab);
+                flow_consume_gen<flow_class_V(1), 8, HAS_SYN>(a, h, stage, ct, etab);
             else
-                flow_consume_gen<1, 12, HAS_SYN>(a, h, stage, ct, etab);
+                flow_consume_gen<flow_class_V(2), 12, HAS_SYN>(a, h, stage, ct, etab);
             fence_proxy_async_smem();  // this thread's STS -> visible to the bulk-store engine
             __syncwarp();
             if (lane == 0) mbar_arrive(&done[s]);

@@ -415,7 +415,7 @@ static int ensure_flow(qcl_state *st, int counters) {
         for (int s = 0; s < p->S; s++) {
             const int d = p->h_slots[s].degree;
             const uint32_t cls = d <= 4 ? 0 : d <= 8 ? 1 : 2;
-            const int KT = kFlowConsumers * 32 * flow_class_V(cls) / st->W;
+            const int KT = flow_KT((int)cls, st->W);
             nkb[s] = (int)cdiv(p->z, KT);
             stab[s].x = (uint32_t)p->h_slots[s].edge_off | ((uint32_t)d << 16) | (cls << 24);
             stab[s].y = (uint32_t)off;
@@ -441,13 +441,15 @@ static int ensure_flow(qcl_state *st, int counters) {
         // cudaMemcpy from pageable memory may return before its DMA lands, and the state's
         // stream does not synchronise with the legacy stream: wait for the uploads here
         CK(cudaDeviceSynchronize());
-        // ring depth: QCL_FLOW_STAGES (default 3), reduced until two CTAs fit per SM
-        static int want = env_int("QCL_FLOW_STAGES", 3);
+        // ring depth: QCL_FLOW_STAGES (default 3 with two CTAs per SM, 5 with one), reduced
+        // until the CTAs fit
+        static int want = env_int("QCL_FLOW_STAGES", kFlowCtasPerSm == 1 ? 5 : 3);
         int stages = std::max(2, std::min(want, kFlowMaxStages));
         int sms = 0, per_sm = 0, max_smem = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device));
         CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device));
-        while (stages > 2 && flow_smem_bytes(p->S, p->E, stages) * 2 + 2048 > 233472) stages--;
+        while (stages > 2 && flow_smem_bytes(p->S, p->E, stages) * kFlowCtasPerSm + 1024 * kFlowCtasPerSm > 233472)
+            stages--;
         const size_t smem = flow_smem_bytes(p->S, p->E, stages);
         if ((int64_t)smem > max_smem) {
             st->f_grid = -1;  // tables too large: the per-layer engine runs instead

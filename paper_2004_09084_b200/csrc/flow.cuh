@@ -41,6 +41,9 @@
 
 #include "pipeline.cuh"
 
+#ifndef QCL_FLOW_PAR_FLAGS
+#define QCL_FLOW_PAR_FLAGS 1
+#endif
 #ifndef QCL_FLOW_STAGE_KB
 #define QCL_FLOW_STAGE_KB 32
 #endif
@@ -500,9 +503,23 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                     a0 -= (a0 >= a.z) ? a.z : 0;
                     const int b = a0 + h.kt - 1;
                     const int hi = min(b, a.z - 1);
+#if QCL_FLOW_PAR_FLAGS
+                    // load the (usually two) covering flags together, then poll only stale ones
+                    const int lo = a0 / KTp, nlo = hi / KTp - lo + 1;
+                    const int nfl = nlo + (b >= a.z ? (b - a.z) / KTp + 1 : 0);
+                    int fv[4];
+#pragma unroll
+                    for (int m = 0; m < 4; m++)
+                        if (m < nfl) fv[m] = ld_relaxed(fl + (m < nlo ? lo + m : m - nlo));
+#pragma unroll
+                    for (int m = 0; m < 4; m++)
+                        if (m < nfl && fv[m] < need) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo), need);
+                    for (int m = 4; m < nfl; m++) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo), need);
+#else
                     for (int kb = a0 / KTp; kb <= hi / KTp; kb++) polls += spin_until(fl + kb, need);
                     if (b >= a.z)
                         for (int kb = 0; kb <= (b - a.z) / KTp; kb++) polls += spin_until(fl + kb, need);
+#endif
                 }
                 FLOW_TICK(2);
                 if (prof) {

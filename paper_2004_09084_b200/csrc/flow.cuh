@@ -41,8 +41,8 @@
 
 #include "pipeline.cuh"
 
-#ifndef QCL_FLOW_PAR_FLAGS
-#define QCL_FLOW_PAR_FLAGS 1
+#ifndef QCL_FLOW_PREFETCH_FLAGS
+#define QCL_FLOW_PREFETCH_FLAGS 0
 #endif
 #ifndef QCL_FLOW_STAGE_KB
 #define QCL_FLOW_STAGE_KB 32
@@ -446,6 +446,42 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         }
         int sentinels = 0;
         unsigned long long n_waited = 0, n_polls = 0, n_tiles = 0;
+        // lane j < d: the flags of the previous writer of edge j's column covering this
+        // tile's offsets (kb in [lo, lo + nlo) and, past the wrap at z, [0, nfl - nlo))
+        auto flag_plan = [&](const FlowHdr &h, const int *&fl, int &need, int &lo, int &nlo, int &nfl) {
+            nfl = 0;
+            if (lane >= h.d) return;
+            const uint32_t dy = etab[h.edge_off + lane].y;
+            need = h.t + 1 - (int)((dy >> 15) & 1);
+            if (need <= 0) return;
+            const uint2 pst = stab[dy & 0x7fff];
+            const int KTp = flow_KT(pst.x >> 24, W);
+            fl = a.flags + (size_t)h.g * a.nkb_total + pst.y;
+            int a0 = h.k0 + (int)(dy >> 16);
+            a0 -= (a0 >= a.z) ? a.z : 0;
+            const int b = a0 + h.kt - 1;
+            lo = a0 / KTp;
+            nlo = min(b, a.z - 1) / KTp - lo + 1;
+            nfl = nlo + (b >= a.z ? (b - a.z) / KTp + 1 : 0);
+        };
+        auto resolve = [&](int item, int2 e) {
+            FlowHdr h;
+            h.t = item / a.sweep_items;
+            h.slot = e.x & 0xffff;
+            h.g = e.x >> 16;
+            const uint2 st = stab[h.slot];
+            h.edge_off = st.x & 0xffff;
+            h.d = (st.x >> 16) & 0xff;
+            h.cls = st.x >> 24;
+            const int KT = flow_KT(h.cls, W);
+            h.k0 = e.y * KT;
+            h.kt = min(KT, a.z - h.k0);
+            return h;
+        };
+        // flags of the next item, loaded while this one is queued (QCL_FLOW_PREFETCH_FLAGS);
+        // a prefetched value that satisfies a dependency is a valid observation (flags only
+        // grow), a stale one is simply polled again
+        int pf_item = -1, pf_fv[4];
         for (int it = 0, q = 0, ph = 0;; it++) {
             if (prof) tc = clock64();
             if (it >= kFlowQueue) mbar_wait_sleep(&qfree[q], ph ^ 1);
@@ -471,55 +507,30 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                     if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
                 }
                 FLOW_TICK(1);
-                FlowHdr h;
-                h.t = item / a.sweep_items;
-                h.slot = e.x & 0xffff;
-                h.g = e.x >> 16;
-                const uint2 st = stab[h.slot];
-                h.edge_off = st.x & 0xffff;
-                h.d = (st.x >> 16) & 0xff;
-                h.cls = st.x >> 24;
-                const int KT = flow_KT(h.cls, W);
-                h.k0 = e.y * KT;
-                h.kt = min(KT, a.z - h.k0);
+                const FlowHdr h = resolve(item, e);
                 if (a.gactive && !a.gactive[h.g]) {
                     // every frame of this lane group has converged: its outputs are frozen,
                     // so the tile is not updated -- only released for the group's later tiles
                     __syncwarp();
-                    if (lane == 0) st_release(a.flags + (size_t)h.g * a.nkb_total + st.y + e.y, h.t + 1);
+                    if (lane == 0) st_release(a.flags + (size_t)h.g * a.nkb_total + stab[h.slot].y + e.y, h.t + 1);
+                    pf_item = -1;
                     goto next_item;
                 }
-                // wait for the previous writers of every column of this tile
+                // wait for the previous writers of every column of this tile: all covering
+                // flags of an edge are loaded together (one round trip), only stale ones polled
                 int polls = 0;
-                const int *fg = a.flags + (size_t)h.g * a.nkb_total;
-                for (int j = lane; j < h.d; j += 32) {
-                    const uint32_t dy = etab[h.edge_off + j].y;
-                    const int need = h.t + 1 - (int)((dy >> 15) & 1);
-                    if (need <= 0) continue;
-                    const uint2 pst = stab[dy & 0x7fff];
-                    const int KTp = flow_KT(pst.x >> 24, W);
-                    const int *fl = fg + pst.y;
-                    int a0 = h.k0 + (int)(dy >> 16);
-                    a0 -= (a0 >= a.z) ? a.z : 0;
-                    const int b = a0 + h.kt - 1;
-                    const int hi = min(b, a.z - 1);
-#if QCL_FLOW_PAR_FLAGS
-                    // load the (usually two) covering flags together, then poll only stale ones
-                    const int lo = a0 / KTp, nlo = hi / KTp - lo + 1;
-                    const int nfl = nlo + (b >= a.z ? (b - a.z) / KTp + 1 : 0);
-                    int fv[4];
+                {
+                    const int *fl = nullptr;
+                    int need = 0, lo = 0, nlo = 0, nfl = 0, fv[4];
+                    flag_plan(h, fl, need, lo, nlo, nfl);
+                    const bool have = pf_item == item;
 #pragma unroll
                     for (int m = 0; m < 4; m++)
-                        if (m < nfl) fv[m] = ld_relaxed(fl + (m < nlo ? lo + m : m - nlo));
+                        if (m < nfl) fv[m] = have ? pf_fv[m] : ld_relaxed(fl + (m < nlo ? lo + m : m - nlo));
 #pragma unroll
                     for (int m = 0; m < 4; m++)
                         if (m < nfl && fv[m] < need) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo), need);
                     for (int m = 4; m < nfl; m++) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo), need);
-#else
-                    for (int kb = a0 / KTp; kb <= hi / KTp; kb++) polls += spin_until(fl + kb, need);
-                    if (b >= a.z)
-                        for (int kb = 0; kb <= (b - a.z) / KTp; kb++) polls += spin_until(fl + kb, need);
-#endif
                 }
                 FLOW_TICK(2);
                 if (prof) {
@@ -532,6 +543,17 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 if (lane == 0) {
                     hq[q] = h;
                     mbar_arrive(&ready[q]);  // release: the loader's bulk reads follow these polls
+                }
+                pf_item = -1;
+                if (QCL_FLOW_PREFETCH_FLAGS && n1 < a.item_end) {  // the next item's flags
+                    const FlowHdr hn = resolve(n1, r1);
+                    const int *fl = nullptr;
+                    int need = 0, lo = 0, nlo = 0, nfl = 0;
+                    flag_plan(hn, fl, need, lo, nlo, nfl);
+#pragma unroll
+                    for (int m = 0; m < 4; m++)
+                        if (m < nfl) pf_fv[m] = ld_relaxed(fl + (m < nlo ? lo + m : m - nlo));
+                    pf_item = n1;
                 }
                 FLOW_TICK(3);
             }

@@ -115,6 +115,15 @@ int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms);
 int qcl_state_results(qcl_state *st, uint8_t *words, uint8_t *converged, int64_t *iterations);
 /* The transmitted words of the last synthetic encode-mode fill, (B, n). */
 int qcl_state_truths(qcl_state *st, uint8_t *words);
+/* Frame pool: n_frames device-generated BIAWGN frames (Philox keyed by (seed, snr_idx,
+ * frame), all-zero word, zero syndrome) streamed through the state's lanes with early
+ * termination: a lane whose frame converged or hit max_iterations records the outcome at
+ * its frame index and takes the next frame.  Per-frame outcomes equal the batch decode's;
+ * conv/err are (n_frames) bytes, iters (n_frames) int64; err = frame error (bench.py:236-237).
+ * Flow engine only (FP32). */
+int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, int64_t snr_idx, int64_t first_frame,
+                          int64_t n_frames, double snr, uint8_t *conv, int64_t *iters, uint8_t *err,
+                          float *elapsed_ms);
 /* Campaign frame errors (reference bench.py:236-237): mismatch[b] = 1 when the decoded
  * word of frame b (after qcl_state_decode) differs from its transmitted word -- the
  * encode-mode truths of the last synthetic fill, else the all-zero word.  (B) bytes. */

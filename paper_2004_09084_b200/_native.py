@@ -64,6 +64,7 @@ _SIGNATURES = {
     "qcl_state_kernel_stats": ([_vp, _vp, _vp, _vp], ctypes.c_int),
     "qcl_state_set_engine": ([_vp, _i32], ctypes.c_int),
     "qcl_state_frame_errors": ([_vp, _vp], ctypes.c_int),
+    "qcl_state_decode_pool": ([_vp, _vp, ctypes.c_uint64, _i64, _i64, _i64, _dbl, _vp, _vp, _vp, _vp], ctypes.c_int),
     "qcl_phi": ([_vp, _i64, _dbl, _dbl, _i32, _i32, _vp], ctypes.c_int),
     "qcl_state_set_syndrome_hint": ([_vp, _vp, _i32], ctypes.c_int),
     "qcl_state_decode_async": ([_vp, _vp], ctypes.c_int),
@@ -244,6 +245,16 @@ class State:
         w = np.empty((self.batch, self.plan.n), np.uint8)
         call("qcl_state_truths", self.handle, ptr(w))
         return w
+
+    def decode_pool(self, qcfg, seed, snr_idx, first_frame, n_frames, snr):
+        """Frame pool (qcl_state_decode_pool): per-frame (converged, iterations, frame error), ms."""
+        conv = np.empty(n_frames, np.uint8)
+        err = np.empty(n_frames, np.uint8)
+        iters = np.empty(n_frames, np.int64)
+        ms = ctypes.c_float(0)
+        call("qcl_state_decode_pool", self.handle, ctypes.byref(qcfg), int(seed) & (2**64 - 1), int(snr_idx),
+             int(first_frame), int(n_frames), float(snr), ptr(conv), ptr(iters), ptr(err), ctypes.byref(ms))
+        return conv.astype(bool), iters, err.astype(bool), float(ms.value)
 
     def frame_errors(self):
         """Per frame: decoded word differs from the transmitted one (qcl_state_frame_errors)."""

@@ -21,6 +21,12 @@ Extra ``CampaignConfig`` fields (all optional, reference behaviour by default):
   (``tests/test_acceptance.py:194,236`` form), not bit-for-bit.
 * ``devices`` -- GPU ordinals; each batch is split into contiguous slices, one per GPU
   and host thread (``np.array_split`` as ``bench.py:143``), no collective.  Default ``(0,)``.
+* ``frame_pool`` -- device channel with early termination on the FP32 flow engine: the
+  whole SNR point's frames stream through ``batch_size`` lanes per GPU, a lane taking the
+  next frame as soon as its frame converges or hits the cap (``qcl_state_decode_pool``),
+  so one slow frame no longer holds a batch to the cap.  Per-frame outcomes, hence FER and
+  average iterations, are identical to the batched decode; only the timing changes.
+  Default ``True`` (used whenever it applies).
 
 Timing follows ``bench.py:230-234``: wall-clock around the decode only (LLR generation
 and error counting are outside), so ``throughput_mbits_per_s`` is frames * n / decode
@@ -99,6 +105,7 @@ class CampaignConfig:
     precision: str = "fp32"
     channel: str = "host"
     devices: tuple = (0,)
+    frame_pool: bool = True
 
     def __post_init__(self):
         object.__setattr__(self, "snr_list", tuple(float(s) for s in self.snr_list))
@@ -198,6 +205,7 @@ def _campaign_metadata(cfg, base, desc, schedule):
         "precision": cfg.precision,
         "channel": cfg.channel,
         "devices": list(cfg.devices),
+        "frame_pool": _uses_pool(cfg),
     }
     return meta
 
@@ -296,6 +304,34 @@ class _DeviceChannelRunner:
             self.pool.shutdown()
 
 
+def _uses_pool(cfg):
+    return (cfg.frame_pool and cfg.channel == "device" and cfg.early_termination and not cfg.encode_mode
+            and cfg.precision == "fp32")
+
+
+class _PoolRunner(_DeviceChannelRunner):
+    """All frames of an SNR point through ``batch_size`` lanes per GPU (frame pool)."""
+
+    def point(self, snr_idx, chan, frames):
+        sizes = [len(c) for c in np.array_split(np.arange(frames), len(self.plans))]
+        jobs, first = [], 0
+        for dev, size in enumerate(sizes):
+            if size:
+                jobs.append((dev, snr_idx, chan.snr, first, size))
+            first += size
+
+        def run(job):
+            dev, si, snr, f0, count = job
+            st = self._state(dev, min(self.cfg.batch_size, count))
+            t0 = time.perf_counter()
+            conv, iters, err, _ = st.decode_pool(self.qcfg, self.cfg.seed, si, f0, count, snr)
+            return conv, err, iters, time.perf_counter() - t0
+
+        parts = list(self.pool.map(run, jobs)) if self.pool else [run(j) for j in jobs]
+        return (np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]),
+                np.concatenate([p[2] for p in parts]), max(p[3] for p in parts))
+
+
 def run_campaign(cfg):
     """Measure FER/iterations/latency/throughput at every SNR point (``bench.py:188-258``)."""
     base = load_base_matrix(cfg.matrix_path)
@@ -309,7 +345,8 @@ def run_campaign(cfg):
     n = desc.block_length
     m = desc.n_checks
     frames = cfg.frames_per_point
-    runner_cls = _HostChannelRunner if cfg.channel == "host" else _DeviceChannelRunner
+    pool = _uses_pool(cfg)
+    runner_cls = _PoolRunner if pool else (_HostChannelRunner if cfg.channel == "host" else _DeviceChannelRunner)
     runner = runner_cls(cfg, index, schedule, dcfg, n, m, rows)
 
     cells = []
@@ -319,7 +356,11 @@ def run_campaign(cfg):
             errors = 0
             iterations_total = 0
             wall = 0.0
-            for start in range(0, frames, cfg.batch_size):
+            if pool:
+                converged, mismatch, iterations, wall = runner.point(snr_idx, chan, frames)
+                errors += int((~converged).sum()) + int((converged & mismatch).sum())
+                iterations_total += int(iterations.sum())
+            for start in range(0, 0 if pool else frames, cfg.batch_size):
                 batch = min(cfg.batch_size, frames - start)
                 converged, mismatch, iterations, dt = runner.batch(snr_idx, chan, start, batch)
                 wall += dt

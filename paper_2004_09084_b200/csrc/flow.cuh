@@ -93,7 +93,8 @@ struct FlowArgs {
     const uint2 *edge_tab;   // [E]
     const int2 *items;       // per item of one sweep: {slot | g << 16, kb}
     int32_t sweep_items;     // items per sweep
-    int32_t item_begin, item_end;  // global item range of this launch (t * sweep_items + ...)
+    int32_t item_begin, item_end;  // item range of this launch, relative to sweep t_base
+    int32_t t_base;                // global sweep index of item 0 (flags count global sweeps)
     int *counter;            // claim counter of this launch (zeroed before it)
     int *flags;              // [G][nkb_total] iterations completed per tile
     int32_t nkb_total;
@@ -106,6 +107,7 @@ struct FlowArgs {
     const int *n_active;  // early termination: skip the launch once every frame converged
     const uint8_t *gactive;  // early termination: lane groups with an active frame (others skipped)
     int32_t defer_last;      // >= 0: degree-1 edges keep q in the L slot and no R until sweep defer_last
+    const uint32_t *fresh;   // frame pool: [G] lanes that start a new frame this sweep (r_old = 0)
     unsigned long long *stats;  // optional instrumentation (QCL_FLOW_STATS)
     double clip, eps;
     double mag_max;             // FP32 bound on |r| (LayerArgs::mag_max)
@@ -227,6 +229,7 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
     int par[V];
     const uint32_t dmask = flow_deferred_mask(a, h, etab);
     const bool last = h.t == a.defer_last;
+    const uint32_t fresh_lanes = a.fresh ? a.fresh[h.g] : 0u;
     if (HAS_SYN) {
         const uint8_t *sp = a.syn + ((((int64_t)h.g * a.S + h.slot) * a.z + h.k0 + ci) << a.lw) + w0;
 #pragma unroll
@@ -245,6 +248,11 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
                 for (int v = 0; v < V; v++) q[j][v] = lv[v];
             } else {
                 *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+                if (fresh_lanes) {  // frame pool: lanes that just took a new frame have r_old = 0
+#pragma unroll
+                    for (int v = 0; v < V; v++)
+                        if ((fresh_lanes >> (w0 + v)) & 1) rv[v] = 0.0f;
+                }
 #pragma unroll
                 for (int v = 0; v < V; v++) q[j][v] = clampT(lv[v] - rv[v], clip);
             }
@@ -303,6 +311,7 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
     using VT = typename Vec<float, V>::type;
     float q[D][V], t[D][V];
     int par[V];
+    const uint32_t fresh_lanes = a.fresh ? a.fresh[h.g] : 0u;
     const uint32_t dmask = flow_deferred_mask(a, h, etab);
     const bool last = h.t == a.defer_last;
     if (HAS_SYN) {
@@ -327,6 +336,7 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
             const bool dj = (dmask >> j) & 1;  // the L slot already holds q
 #pragma unroll
             for (int v = 0; v < V; v++) {
+                if ((fresh_lanes >> (w0 + v)) & 1) rv[v] = 0.0f;  // frame pool: new frame, r_old = 0
                 q[j][v] = dj ? lv[v] : clampT(lv[v] - rv[v], clip);
                 t[j][v] = sd_t(q[j][v]);
                 par[v] ^= (q[j][v] < 0.0f);
@@ -466,7 +476,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         };
         auto resolve = [&](int item, int2 e) {
             FlowHdr h;
-            h.t = item / a.sweep_items;
+            h.t = a.t_base + item / a.sweep_items;
             h.slot = e.x & 0xffff;
             h.g = e.x >> 16;
             const uint2 st = stab[h.slot];

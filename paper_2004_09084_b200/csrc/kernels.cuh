@@ -432,19 +432,13 @@ __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
 // Lane groups whose frames have all converged (early termination) are skipped when
 // gact != nullptr: their outputs were frozen at convergence, so nothing observable
 // depends on their later state.
-// signs[v][g]: bit w = (L[g][v][w] < 0), i.e. all lane groups of a variable side by side,
-// so one syndrome-check thread reads every group's sign word of a variable in one go.
+// Sign word of variable v of group g (element i = g*n + v): bit w = (L[g][v][w] < 0).
 template <typename T>
-__global__ void __launch_bounds__(kBlock) sign_pack_kernel(const T *L, int64_t Gn, int lw, uint32_t *signs, int64_t n,
-                                                           const uint8_t *gact) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over G * n: one variable of one group
-    if (i >= Gn) return;
-    const int64_t g = i / n, v = i - g * n;
-    if (gact && !gact[g]) return;
+__device__ __forceinline__ uint32_t sign_word(const T *L, int64_t i, int lw) {
     const int W = 1 << lw;
     const T *p = L + (i << lw);
     uint32_t m = 0;
-    if (sizeof(T) == 4 && (W & 3) == 0) {  // W lanes = W/4 coalesced 16-byte loads
+    if (sizeof(T) == 4 && (W & 3) == 0) {
         for (int w = 0; w < W; w += 4) {
             const float4 x = __ldcg(reinterpret_cast<const float4 *>(p + w));
             m |= ((uint32_t)(x.x < 0.0f) | ((uint32_t)(x.y < 0.0f) << 1) | ((uint32_t)(x.z < 0.0f) << 2) |
@@ -453,6 +447,19 @@ __global__ void __launch_bounds__(kBlock) sign_pack_kernel(const T *L, int64_t G
     } else {
         for (int w = 0; w < W; w++) m |= (uint32_t)(__ldcg(p + w) < (T)0) << w;
     }
+    return m;
+}
+
+// signs[v][g]: bit w = (L[g][v][w] < 0), i.e. all lane groups of a variable side by side,
+// so one syndrome-check thread reads every group's sign word of a variable in one go.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) sign_pack_kernel(const T *L, int64_t Gn, int lw, uint32_t *signs, int64_t n,
+                                                           const uint8_t *gact) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over G * n: one variable of one group
+    const int64_t g = i < Gn ? i / n : -1, v = i - g * n;
+    const bool live = i < Gn && (!gact || gact[g]);
+    if (!live) return;
+    const uint32_t m = sign_word(L, i, lw);
     signs[v * (Gn / n) + g] = m;
 }
 
@@ -746,6 +753,116 @@ __global__ void __launch_bounds__(kBlock) frame_mismatch_kernel(const uint8_t *w
             bad |= w[i] != (t ? t[i] : 0);
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0) mismatch[b] = 1;
+}
+
+// ---- frame pool (qcl_state_decode_pool): lanes refilled as their frames finish --------
+//
+// Campaign decodes with early termination run a stream of frames through the lanes of one
+// state: a lane whose frame converged (or hit the iteration cap) records the frame's
+// outcome and takes the next frame, so a batch no longer runs to the cap for one slow
+// frame.  Per-frame outcomes are unchanged: frames are independent, every frame runs the
+// same layered sweeps from its own new_state (a refilled lane starts from L = clip(llr),
+// and the flow kernel treats its old messages as zero in its first sweep).
+
+// lane_any[g] |= bit w when the hard decision of lane w of group g has any bit set (the
+// all-zero word is the transmitted one: a converged frame is in error iff a bit is set).
+// Grid-stride over variables (variable-major sign words, G per variable), per-thread OR
+// accumulators, then warp and block reductions: one atomic per group and block.
+__global__ void __launch_bounds__(kBlock) lane_any_kernel(const uint32_t *signs, int64_t n, int G,
+                                                          const uint8_t *gact, uint32_t *lane_any) {
+    __shared__ uint32_t s_acc[32];
+    for (int g0 = 0; g0 < G; g0 += 32) {
+        const int cnt = min(32, G - g0);
+        if (threadIdx.x < 32) s_acc[threadIdx.x] = 0;
+        __syncthreads();
+        uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int c0 = 0; c0 < cnt; c0 += 8) {
+            for (int c = 0; c < 8; c++) acc[c] = 0;
+            for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+                const uint32_t *row = signs + v * G + g0 + c0;
+#pragma unroll
+                for (int c = 0; c < 8; c++)
+                    if (c0 + c < cnt) acc[c] |= __ldg(row + c);
+            }
+#pragma unroll
+            for (int c = 0; c < 8; c++) {
+                const uint32_t m = __reduce_or_sync(0xffffffffu, acc[c]);
+                if (m && (threadIdx.x & 31) == 0) atomicOr(&s_acc[c0 + c], m);
+            }
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < cnt && s_acc[threadIdx.x] && (!gact || gact[g0 + threadIdx.x]))
+            atomicOr(lane_any + g0 + threadIdx.x, s_acc[threadIdx.x]);
+        __syncthreads();
+    }
+}
+
+// After sweep t: per lane, count the sweep, and finish the frame when its syndrome is met or
+// the cap is reached (outcome recorded at its frame index); hand the lane the next frame
+// (fresh for the next sweep, queued for the refill kernel) or retire it.
+__global__ void pool_update_kernel(int64_t Bp, int lw, int max_iter, const uint32_t *unsat_mask,
+                                   const uint32_t *lane_any, int64_t first_frame, int64_t n_frames,
+                                   int64_t *lane_frame, int32_t *lane_iter, uint8_t *active, int *n_active,
+                                   uint8_t *out_conv, int64_t *out_iters, uint8_t *out_err, int32_t *counts,
+                                   int32_t *refill, uint32_t *fresh) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= Bp) return;
+    const int64_t f = lane_frame[b];
+    if (f < 0) return;
+    const int it = ++lane_iter[b];
+    const bool conv = !lane_unsat(unsat_mask, b, lw);
+    if (!conv && it < max_iter) return;
+    const int64_t j = f - first_frame;
+    out_conv[j] = conv;
+    out_iters[j] = conv ? it : max_iter;
+    out_err[j] = !conv || ((lane_any[b >> lw] >> (b & ((1 << lw) - 1))) & 1u);
+    const int64_t nf = atomicAdd(counts + 1, 1);
+    if (nf < n_frames) {
+        lane_frame[b] = first_frame + nf;
+        lane_iter[b] = 0;
+        refill[atomicAdd(counts, 1)] = (int32_t)b;
+        atomicOr(fresh + (b >> lw), 1u << (b & ((1 << lw) - 1)));
+    } else {
+        lane_frame[b] = -1;
+        active[b] = 0;
+        atomicSub(n_active, 1);
+    }
+}
+
+// New frames for the lanes in refill[0..counts[0]): Philox LLRs exactly as
+// synth_llr_kernel (same (seed, snr_idx, frame) keying, all-zero word) into llr and
+// L = clip(llr) + 0 (new_state).  Refill slots are strided over blockIdx.y, so the grid is
+// small when (as in most sweeps) few or no lanes are refilled.
+__device__ __forceinline__ void pool_refill_quad(int64_t b, int64_t qv, const int64_t *lane_frame, int64_t n, int lw,
+                                                 uint64_t seed, uint32_t snr_idx, double sigma, double sigma2,
+                                                 double clip, float *llr, float *L) {
+    const int W = 1 << lw;
+    const int64_t g = b >> lw, w = b & (W - 1);
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    const uint64_t frame = (uint64_t)lane_frame[b];
+    u32x4 ctr{(uint32_t)qv, (uint32_t)frame, (uint32_t)(frame >> 32), snr_idx & 0x7fffffffu};
+    double nz[4];
+    normals4(philox4x32_10(ctr, k0, k1), nz);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int64_t v = qv * 4 + j;
+        if (v >= n) break;
+        const double r = 1.0 + sigma * nz[j];
+        const float val = (float)(2.0 * r / sigma2);
+        const int64_t idx = ((g * n + v) << lw) + w;
+        llr[idx] = val;
+        L[idx] = (float)clampT((double)val, clip) + 0.0f;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) pool_refill_kernel(const int32_t *counts, const int32_t *refill,
+                                                             const int64_t *lane_frame, int64_t n, int lw,
+                                                             uint64_t seed, uint32_t snr_idx, double sigma,
+                                                             double sigma2, double clip, float *llr, float *L) {
+    const int64_t qv = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (qv >= (n + 3) / 4) return;
+    for (int slot = blockIdx.y; slot < counts[0]; slot += gridDim.y)
+        pool_refill_quad(refill[slot], qv, lane_frame, n, lw, seed, snr_idx, sigma, sigma2, clip, llr, L);
 }
 
 __global__ void phi_array_kernel(const double *x, int64_t cnt, double eps, double clip, int prec, double *out) {

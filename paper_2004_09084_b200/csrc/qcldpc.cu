@@ -128,6 +128,14 @@ struct qcl_state {
     int64_t f_sweep_items = 0;
     int32_t f_nkb_total = 0, f_counter_cap = 0, f_grid = 0, f_stages = 3;
     bool flow_decode = false;  // this decode runs on the flow engine
+    // frame pool (qcl_state_decode_pool): per lane frame index / iterations, refill list
+    bool pool_active = false;
+    int64_t *pframe = nullptr;     // [Bp] frame decoded by the lane, -1 idle
+    int32_t *piter = nullptr;      // [Bp] iterations of the lane's current frame
+    uint32_t *pfresh = nullptr;    // [G] lanes that start a new frame in the next sweep
+    uint32_t *plane_any = nullptr; // [G] lanes whose hard decision has a set bit
+    int32_t *prefill = nullptr;    // [Bp] lanes to refill this sweep
+    int32_t *pcount = nullptr;     // [0] refills this sweep, [1] frames handed out
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sweep_events;
 };
 
@@ -496,8 +504,9 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.edge_tab = p->fedge_tab;
     a.items = st->fitems;
     a.sweep_items = (int32_t)st->f_sweep_items;
-    a.item_begin = (int32_t)(t0 * st->f_sweep_items);
-    a.item_end = (int32_t)((t0 + T) * st->f_sweep_items);
+    a.item_begin = 0;
+    a.item_end = (int32_t)(T * st->f_sweep_items);
+    a.t_base = t0;
     a.counter = st->fcounters + counter;
     a.flags = st->fflags;
     a.nkb_total = st->f_nkb_total;
@@ -514,6 +523,7 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.n_active = et ? st->n_active : nullptr;
     a.gactive = et ? st->gactive : nullptr;
     a.defer_last = defer_last;
+    a.fresh = st->pool_active ? st->pfresh : nullptr;
     a.stats = st->fstats;
     a.clip = clip;
     a.eps = eps;
@@ -914,6 +924,8 @@ int qcl_state_destroy(qcl_state *st) {
                       (void *)st->unsat, (void *)st->signs, (void *)st->synpack, (void *)st->active, (void *)st->gactive,
                       (void *)st->take, (void *)st->iters,
                       (void *)st->n_active, (void *)st->truths, st->staging, (void *)st->fslot_tab,
+                      (void *)st->pframe, (void *)st->piter, (void *)st->pfresh, (void *)st->plane_any,
+                      (void *)st->prefill, (void *)st->pcount,
                       (void *)st->fitems, (void *)st->fflags, (void *)st->fcounters, (void *)st->fstats})
         if (ptr) cudaFree(ptr);
     if (st->h_n_active) cudaFreeHost(st->h_n_active);
@@ -1403,6 +1415,118 @@ int qcl_state_decode(qcl_state *st, const qcl_config *cfg, float *elapsed_ms) {
     int rc = enqueue_decode(st, cfg, true);
     if (rc) return rc;
     return finish_decode(st, elapsed_ms);
+}
+
+static int sms_of(const qcl_state *st) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st->plan->device);
+    return sms;
+}
+
+// Frame pool: n_frames device-generated frames (all-zero word, zero syndrome) streamed
+// through the state's lanes with early termination (kernels.cuh, "frame pool").  Outcomes
+// land at their frame index: conv, iters, err (frame error as bench.py:236-237).
+int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, int64_t snr_idx, int64_t first_frame,
+                          int64_t n_frames, double snr, uint8_t *conv, int64_t *iters, uint8_t *err,
+                          float *elapsed_ms) {
+    if (!st || !conv || !iters || !err) return fail(QCL_EVALUE, "NULL argument");
+    int rc = validate_cfg(cfg);
+    if (rc) return rc;
+    if (cfg->precision != st->prec) return fail(QCL_EVALUE, "config precision differs from the state's");
+    if (!cfg->early_termination) return fail(QCL_EVALUE, "the frame pool needs early termination");
+    if (n_frames < 1) return fail(QCL_EVALUE, "n_frames must be at least 1");
+    if (!(snr > 0)) return fail(QCL_EVALUE, "snr must be positive");
+    if (!use_flow(st)) return fail(QCL_EUNSUP, "the frame pool runs on the flow engine (FP32, engine 4)");
+    const qcl_plan *p = st->plan;
+    CK(cudaSetDevice(p->device));
+    if ((rc = ensure_flow(st, 2))) return rc;
+    if (!use_flow(st)) return fail(QCL_EUNSUP, "the frame pool runs on the flow engine (FP32, engine 4)");
+    auto al = [&](void **ptr, size_t bytes) -> int {
+        if (*ptr) return QCL_OK;
+        CK(cudaMalloc(ptr, std::max<size_t>(bytes, 16)));
+        return QCL_OK;
+    };
+    if ((rc = al((void **)&st->pframe, sizeof(int64_t) * st->Bp)) || (rc = al((void **)&st->piter, 4 * st->Bp)) ||
+        (rc = al((void **)&st->pfresh, 4 * st->G)) || (rc = al((void **)&st->plane_any, 4 * st->G)) ||
+        (rc = al((void **)&st->prefill, 4 * st->Bp)) || (rc = al((void **)&st->pcount, 16)))
+        return rc;
+    uint8_t *d_conv = nullptr, *d_err = nullptr;
+    int64_t *d_iters = nullptr;
+    CK(cudaMalloc(&d_conv, n_frames));
+    CK(cudaMalloc(&d_err, n_frames));
+    CK(cudaMalloc(&d_iters, 8 * n_frames));
+    cudaStream_t sm = st->stream;
+    const double sigma2 = 1.0 / snr, sigma = sqrt(sigma2);
+    // the first frames fill the lanes: lanes [0, first) get frames first_frame.. in order
+    const int64_t first = std::min<int64_t>(st->B, n_frames);
+    std::vector<int64_t> h_frame(st->Bp, -1);
+    std::vector<uint8_t> h_active(st->Bp, 0);
+    for (int64_t b = 0; b < first; b++) {
+        h_frame[b] = first_frame + b;
+        h_active[b] = 1;
+    }
+    const int32_t h_count[2] = {0, (int32_t)first};
+    const int h_n_active = (int)first;
+    CK(cudaMemcpyAsync(st->pframe, h_frame.data(), 8 * st->Bp, cudaMemcpyHostToDevice, sm));
+    CK(cudaMemcpyAsync(st->active, h_active.data(), st->Bp, cudaMemcpyHostToDevice, sm));
+    CK(cudaMemcpyAsync(st->pcount, h_count, 8, cudaMemcpyHostToDevice, sm));
+    CK(cudaMemcpyAsync(st->n_active, &h_n_active, sizeof(int), cudaMemcpyHostToDevice, sm));
+    CK(cudaMemsetAsync(st->piter, 0, 4 * st->Bp, sm));
+    CK(cudaMemsetAsync(st->pfresh, 0, 4 * st->G, sm));
+    CK(cudaStreamSynchronize(sm));  // the pageable sources above
+    if ((rc = qcl_state_set_llr_synthetic(st, seed, snr_idx, first_frame, snr, 0))) return rc;
+    st->has_syn = false;
+    CK(cudaEventRecord(st->ev0, sm));
+    if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
+    enqueue_group_active(st);
+    CK(cudaMemsetAsync(st->fflags, 0, sizeof(int) * (size_t)st->G * st->f_nkb_total, sm));
+    st->pool_active = true;
+    st->g_et = true;
+    const unsigned gb = (unsigned)cdiv(st->Bp, kBlock);
+    const unsigned qgrid = (unsigned)cdiv((p->n + 3) / 4, kBlock);
+    // every frame needs at most max_iterations sweeps and the lanes work concurrently
+    const int64_t max_sweeps = (int64_t)cfg->max_iterations * (cdiv(n_frames, st->B) + 1) + 1;
+    for (int64_t t = 0; t < max_sweeps; t++) {
+        CK(cudaMemsetAsync(st->fcounters + (t & 1), 0, sizeof(int), sm));
+        if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, (int)t, 1, (int)(t & 1), true))) break;
+        CK(cudaMemsetAsync(st->pfresh, 0, 4 * st->G, sm));
+        if ((rc = enqueue_check(st, st->gactive))) break;
+        CK(cudaMemsetAsync(st->plane_any, 0, 4 * st->G, sm));
+        lane_any_kernel<<<(unsigned)(2 * sms_of(st)), kBlock, 0, sm>>>(st->signs, p->n, st->G, st->gactive,
+                                                                      st->plane_any);
+        CK(cudaMemsetAsync(st->pcount, 0, sizeof(int32_t), sm));
+        pool_update_kernel<<<gb, kBlock, 0, sm>>>(st->Bp, st->lw, cfg->max_iterations, st->unsat, st->plane_any,
+                                                 first_frame, n_frames, st->pframe, st->piter, st->active,
+                                                 st->n_active, d_conv, d_iters, d_err, st->pcount, st->prefill,
+                                                 st->pfresh);
+        pool_refill_kernel<<<dim3(qgrid, (unsigned)std::min<int64_t>(st->Bp, 8)), kBlock, 0, sm>>>(
+            st->pcount, st->prefill, st->pframe, p->n, st->lw, seed, (uint32_t)snr_idx, sigma, sigma2,
+            cfg->llr_clip, (float *)st->llr, (float *)st->L);
+        enqueue_group_active(st);
+        CK(cudaGetLastError());
+        // stop once every lane retired: the active count is read one sweep behind
+        CK(cudaMemcpyAsync(st->h_flag + (t & 1), st->n_active, sizeof(int), cudaMemcpyDeviceToHost, sm));
+        CK(cudaEventRecord(st->ev_flag[t & 1], sm));
+        if (t >= 1) {
+            CK(cudaEventSynchronize(st->ev_flag[(t - 1) & 1]));
+            if (st->h_flag[(t - 1) & 1] == 0) break;
+        }
+    }
+    st->pool_active = false;
+    CK(cudaEventRecord(st->ev1, sm));
+    if (!rc) {
+        CK(cudaMemcpyAsync(conv, d_conv, n_frames, cudaMemcpyDeviceToHost, sm));
+        CK(cudaMemcpyAsync(err, d_err, n_frames, cudaMemcpyDeviceToHost, sm));
+        CK(cudaMemcpyAsync(iters, d_iters, 8 * n_frames, cudaMemcpyDeviceToHost, sm));
+    }
+    cudaError_t e = cudaStreamSynchronize(sm);
+    if (elapsed_ms && e == cudaSuccess) cudaEventElapsedTime(elapsed_ms, st->ev0, st->ev1);
+    cudaFree(d_conv);
+    cudaFree(d_err);
+    cudaFree(d_iters);
+    if (rc) return rc;
+    CK(e);
+    return QCL_OK;
 }
 
 int qcl_state_decode_async(qcl_state *st, const qcl_config *cfg) {

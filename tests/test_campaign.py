@@ -17,7 +17,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, ROOT
+from conftest import GOLDEN, ROOT, load_code
 
 CASES = ["campaign_demo4x8z32_et50", "campaign_demo4x8z100_noet10", "campaign_demo4x8z32_encode"]
 
@@ -172,3 +172,43 @@ def test_compare_schedules_on_device(gpu, tmp_path):
     cmp = compare_schedules(cfg)
     assert cmp.single_layer_count == 6 and cmp.merged_layer_count < 6
     assert emit_report(cmp, "csv", tmp_path / "cmp.csv").exists()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["campaign_demo4x8z32_et50", "standin_z100_et"])
+def test_frame_pool_matches_batched_decode_per_frame(gpu, name):
+    """The frame pool changes only the timing: FER and average iterations identical to the
+    batched device-channel decode (frames are independent; each runs its own sweeps)."""
+    from paper_2004_09084_b200.campaign import CampaignConfig, run_campaign
+
+    if name == "standin_z100_et":
+        kw = dict(matrix_path=str(ROOT / "codes" / "standin_v2_z100.txt"), snr_list=(0.17, 0.2), max_iterations=40,
+                  early_termination=True, batch_size=16, min_trials=96, seed=5, channel="device")
+        cfg = CampaignConfig(**kw)
+    else:
+        cfg = config_of(golden(name), channel="device", batch_size=32, min_trials=256)
+    a = run_campaign(cfg.__class__(**{**cfg.__dict__, "frame_pool": False}))
+    b = run_campaign(cfg)
+    assert b.metadata["device"]["frame_pool"] and not a.metadata["device"]["frame_pool"]
+    for x, y in zip(a.cells, b.cells):
+        assert x.fer == y.fer and x.avg_iterations == y.avg_iterations, (x, y)
+
+
+@pytest.mark.gpu
+def test_frame_pool_per_frame_outcomes_against_states(gpu):
+    """qcl_state_decode_pool per frame vs one batched decode per frame range."""
+    import paper_2004_09084_b200 as q
+    from paper_2004_09084_b200 import _native
+
+    base, sched, index = load_code("standin_v2_z100")
+    plan = _native.Plan(index, sched, 0)
+    qcfg = _native.make_config(q.DecoderConfig(max_iterations=30, early_termination=True), "fp32")
+    pool = _native.State(plan, 8, "fp32")
+    conv, iters, err, _ = pool.decode_pool(qcfg, 11, 2, 100, 40, 0.19)
+    ref = _native.State(plan, 40, "fp32")
+    ref.set_llr_synthetic(seed=11, snr_idx=2, first_frame=100, snr=0.19)
+    ref.decode(qcfg)
+    _, rconv, riters = ref.results(words=False)
+    rerr = ref.frame_errors()
+    assert np.array_equal(conv, rconv) and np.array_equal(iters, riters)
+    assert np.array_equal(err, ~rconv | rerr)

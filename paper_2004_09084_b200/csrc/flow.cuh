@@ -41,23 +41,11 @@
 
 #include "pipeline.cuh"
 
-#ifndef QCL_FLOW_PREFETCH_FLAGS
-#define QCL_FLOW_PREFETCH_FLAGS 0
-#endif
 #ifndef QCL_FLOW_STAGE_KB
 #define QCL_FLOW_STAGE_KB 32
 #endif
-#ifndef QCL_FLOW_RELAXED_RELEASE
-#define QCL_FLOW_RELAXED_RELEASE 0
-#endif
-#ifndef QCL_FLOW_NOMATH
-#define QCL_FLOW_NOMATH 0
-#endif
 #ifndef QCL_FLOW_QUEUE
 #define QCL_FLOW_QUEUE 2
-#endif
-#ifndef QCL_FLOW_CLAIM_AHEAD
-#define QCL_FLOW_CLAIM_AHEAD 1
 #endif
 
 namespace qcl {
@@ -261,14 +249,6 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
             for (int v = 0; v < V; v++) q[j][v] = 0.0f;
         }
     }
-#if QCL_FLOW_NOMATH  // timing experiment only: data movement without the check-node math
-    if (true) {
-#pragma unroll
-        for (int j = 0; j < D; j++)
-#pragma unroll
-            for (int v = 0; v < V; v++) ph[j][v] = 0.5f * q[j][v];
-    } else
-#endif
     if (D == 4 && h.d == 4) {
         uint32_t sb[V];
 #pragma unroll
@@ -444,16 +424,12 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         // trip is on the tile's critical path.  Holding claimed items is deadlock free:
         // they are larger than the item in hand.  Resolved headers go to the loader warp
         // through a small queue, so dependency polling overlaps the bulk-copy issue.
-        int n2 = 0, n3 = 0;
+        int n2 = 0;
         if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
         int n1 = __shfl_sync(0xffffffffu, n2, 0);
         int2 r1 = make_int2(0, 0);
         if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
         if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
-        if (QCL_FLOW_CLAIM_AHEAD == 2) {  // n2: the item after n1 (broadcast); n3: claim in flight
-            n2 = __shfl_sync(0xffffffffu, n2, 0);
-            if (lane == 0) n3 = a.item_begin + atomicAdd(a.counter, 1);
-        }
         int sentinels = 0;
         unsigned long long n_waited = 0, n_polls = 0, n_tiles = 0;
         // lane j < d: the flags of the previous writer of edge j's column covering this
@@ -488,10 +464,6 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             h.kt = min(KT, a.z - h.k0);
             return h;
         };
-        // flags of the next item, loaded while this one is queued (QCL_FLOW_PREFETCH_FLAGS);
-        // a prefetched value that satisfies a dependency is a valid observation (flags only
-        // grow), a stale one is simply polled again
-        int pf_item = -1, pf_fv[4];
         for (int it = 0, q = 0, ph = 0;; it++) {
             if (prof) tc = clock64();
             if (it >= kFlowQueue) mbar_wait_sleep(&qfree[q], ph ^ 1);
@@ -506,16 +478,9 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 }
                 if (++sentinels == kFlowStorers) break;
             } else {
-                if (QCL_FLOW_CLAIM_AHEAD == 2) {
-                    n1 = n2;
-                    if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
-                    n2 = __shfl_sync(0xffffffffu, n3, 0);
-                    if (lane == 0) n3 = a.item_begin + atomicAdd(a.counter, 1);
-                } else {
-                    n1 = __shfl_sync(0xffffffffu, n2, 0);
-                    if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
-                    if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
-                }
+                n1 = __shfl_sync(0xffffffffu, n2, 0);
+                if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
+                if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
                 FLOW_TICK(1);
                 const FlowHdr h = resolve(item, e);
                 if (a.gactive && !a.gactive[h.g]) {
@@ -523,7 +488,6 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                     // so the tile is not updated -- only released for the group's later tiles
                     __syncwarp();
                     if (lane == 0) st_release(a.flags + (size_t)h.g * a.nkb_total + stab[h.slot].y + e.y, h.t + 1);
-                    pf_item = -1;
                     goto next_item;
                 }
                 // wait for the previous writers of every column of this tile: all covering
@@ -533,10 +497,9 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                     const int *fl = nullptr;
                     int need = 0, lo = 0, nlo = 0, nfl = 0, fv[4];
                     flag_plan(h, fl, need, lo, nlo, nfl);
-                    const bool have = pf_item == item;
 #pragma unroll
                     for (int m = 0; m < 4; m++)
-                        if (m < nfl) fv[m] = have ? pf_fv[m] : ld_relaxed(fl + (m < nlo ? lo + m : m - nlo));
+                        if (m < nfl) fv[m] = ld_relaxed(fl + (m < nlo ? lo + m : m - nlo));
 #pragma unroll
                     for (int m = 0; m < 4; m++)
                         if (m < nfl && fv[m] < need) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo), need);
@@ -553,17 +516,6 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 if (lane == 0) {
                     hq[q] = h;
                     mbar_arrive(&ready[q]);  // release: the loader's bulk reads follow these polls
-                }
-                pf_item = -1;
-                if (QCL_FLOW_PREFETCH_FLAGS && n1 < a.item_end) {  // the next item's flags
-                    const FlowHdr hn = resolve(n1, r1);
-                    const int *fl = nullptr;
-                    int need = 0, lo = 0, nlo = 0, nfl = 0;
-                    flag_plan(hn, fl, need, lo, nlo, nfl);
-#pragma unroll
-                    for (int m = 0; m < 4; m++)
-                        if (m < nfl) pf_fv[m] = ld_relaxed(fl + (m < nlo ? lo + m : m - nlo));
-                    pf_item = n1;
                 }
                 FLOW_TICK(3);
             }
@@ -653,14 +605,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             fence_proxy_async_global();
             __syncwarp();
             if (lane == 0) {  // ... before the tile is released to its dependents
-#if QCL_FLOW_RELAXED_RELEASE  // timing experiment only: races (tools/flow_stress.py)
-                asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(a.flags + (size_t)h.g * a.nkb_total +
-                                                                        stab[h.slot].y + h.k0 / KT),
-                             "r"(h.t + 1)
-                             : "memory");
-#else
-                st_release(a.flags + (size_t)h.g * a.nkb_total + stab[h.slot].y + h.k0 / KT, h.t + 1);
-#endif
+st_release(a.flags + (size_t)h.g * a.nkb_total + stab[h.slot].y + h.k0 / KT, h.t + 1);
             }
             if (sprof) acc[3] += clock64() - tc;
         }

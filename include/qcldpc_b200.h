@@ -38,6 +38,10 @@ extern "C" {
 
 #define QCL_PREC_FP32 0 /* performance path: FP32 state, exclusive Phi-sums */
 #define QCL_PREC_FP64 1 /* parity path: FP64 state, reference formula and fold order */
+/* Beyond-parity opt-in: FP32 posteriors, FP16 edge messages (|r| rounded
+ * to FP16 before use: 12 instead of 16 bytes per edge and iteration).  Flow engine only
+ * (engine 4/6, whole sweeps); decisions are NOT bit-identical to FP32/FP64. */
+#define QCL_PREC_FP32_MSG16 2
 
 #define QCL_DTYPE_F64 0
 #define QCL_DTYPE_F32 1

@@ -22,7 +22,7 @@ if os.environ.get("QCL_LIB_VARIANT"):
     LIB_PATH = LIB_PATH.with_name(f"libqcldpc_b200_{os.environ['QCL_LIB_VARIANT']}.so")
 
 QCL_OK, QCL_EVALUE, QCL_ECUDA, QCL_EUNSUP = 0, -1, -2, -3
-PREC = {"fp32": 0, "fp64": 1}
+PREC = {"fp32": 0, "fp64": 1, "fp32-msg16": 2}  # include/qcldpc_b200.h QCL_PREC_*
 DTYPE_F64, DTYPE_F32 = 0, 1
 
 

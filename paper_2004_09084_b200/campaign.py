@@ -9,8 +9,9 @@ decode running on the B200 path.
 
 Extra ``CampaignConfig`` fields (all optional, reference behaviour by default):
 
-* ``precision`` -- ``"fp32"`` (default, the throughput path) or ``"fp64"`` (the parity
-  path: the reference's own formula and summation order).
+* ``precision`` -- ``"fp32"`` (default, the throughput path), ``"fp64"`` (the parity
+  path: the reference's own formula and summation order) or ``"fp32-msg16"`` (opt-in
+  FP16 edge messages, flow engine only; FER is compared statistically).
 * ``channel`` -- ``"host"`` (default): frames from the reference's PCG64 substreams
   (``frame_rng(seed, snr_idx, frame)``, ``channel.py:36-56``), bit-identical LLRs, so FER
   and iteration counts equal the reference campaign's on the parity path.
@@ -306,7 +307,7 @@ class _DeviceChannelRunner:
 
 def _uses_pool(cfg):
     return (cfg.frame_pool and cfg.channel == "device" and cfg.early_termination and not cfg.encode_mode
-            and cfg.precision == "fp32")
+            and cfg.precision in ("fp32", "fp32-msg16"))
 
 
 class _PoolRunner(_DeviceChannelRunner):

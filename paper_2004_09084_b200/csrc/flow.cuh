@@ -41,11 +41,17 @@
 
 #include "pipeline.cuh"
 
+// Tile flags one per 128-byte line: neighbouring tiles' flags are written (release
+// stores) and polled by different CTAs, and sharing a line costs ~7% at 64 codewords and
+// ~30% at 16-32 (tools/flow_batches.sh; the polls of one line queue behind its writes).
+#ifndef QCL_FLAG_STRIDE
+#define QCL_FLAG_STRIDE 32  // ints between consecutive tile flags
+#endif
 #ifndef QCL_FLOW_STAGE_KB
 #define QCL_FLOW_STAGE_KB 32
 #endif
 #ifndef QCL_FLOW_QUEUE
-#define QCL_FLOW_QUEUE 2
+#define QCL_FLOW_QUEUE 1
 #endif
 
 namespace qcl {
@@ -81,8 +87,9 @@ struct FlowArgs {
     const uint2 *edge_tab;   // [E]
     const int2 *items;       // per item of one sweep: {slot | g << 16, kb}
     int32_t sweep_items;     // items per sweep
-    int32_t item_begin, item_end;  // item range of this launch, relative to sweep t_base
-    int32_t t_base;                // global sweep index of item 0 (flags count global sweeps)
+    uint32_t sweep_mul, sweep_shift;  // item / sweep_items == (umulhi(item, mul) + item) >> shift
+    int32_t item_end;        // items of this launch (sweeps x sweep_items)
+    int32_t t_base;          // global sweep index of item 0 (flags count global sweeps)
     int *counter;            // claim counter of this launch (zeroed before it)
     int *flags;              // [G][nkb_total] iterations completed per tile
     int32_t nkb_total;
@@ -113,8 +120,45 @@ __host__ __device__ constexpr int flow_KT(int cls, int W) {
                ? (kFlowConsumers * 32 * flow_class_V(cls) / W)
                : (kFlowStageBytes / (8 * flow_class_D(cls) * W));
 }
+// With the default 32 KB stage the stage cap never binds, so KT = 32 * consumers * V / W
+// is a power of two and every tile index computation is a shift (the integer divisions
+// they replace sat on the scheduler's per-item critical path).
+__host__ __device__ constexpr int flow_ilog2(int x) { return x <= 1 ? 0 : 1 + flow_ilog2(x / 2); }
+__host__ __device__ constexpr bool flow_kt_pow2() {
+    return kFlowConsumers * 32 * flow_class_V(0) * 8 * flow_class_D(0) <= kFlowStageBytes &&
+           kFlowConsumers * 32 * flow_class_V(1) * 8 * flow_class_D(1) <= kFlowStageBytes &&
+           kFlowConsumers * 32 * flow_class_V(2) * 8 * flow_class_D(2) <= kFlowStageBytes;
+}
+// log2 KT (flow_kt_pow2() builds only)
+__device__ __forceinline__ int flow_kt_log2(int cls, int lw) {
+    return (cls == 0 ? flow_ilog2(kFlowConsumers * 32 * flow_class_V(0))
+                     : cls == 1 ? flow_ilog2(kFlowConsumers * 32 * flow_class_V(1))
+                                : flow_ilog2(kFlowConsumers * 32 * flow_class_V(2))) -
+           lw;
+}
+// checks per tile on the device
+__device__ __forceinline__ int flow_kt(int cls, int W, int lw) {
+    if constexpr (flow_kt_pow2()) return 1 << flow_kt_log2(cls, lw);
+    return flow_KT(cls, W);
+}
+// tile index of check offset k (k / KT)
+__device__ __forceinline__ int flow_kb_of(int k, int cls, int W, int lw) {
+    if constexpr (flow_kt_pow2()) return k >> flow_kt_log2(cls, lw);
+    return k / flow_KT(cls, W);
+}
 __host__ __device__ constexpr size_t flow_smem_bytes(int S, int E, int stages) {
     return ((kFlowHeadBytes + 8 * (size_t)(S + E) + 127) / 128) * 128 + (size_t)stages * kFlowStageBytes;
+}
+
+// item / sweep_items without a division (item < 2^31, multiplier from flow_sweep_divisor)
+__device__ __forceinline__ int flow_sweep_of(const FlowArgs &a, int item) {
+    return (int)((__umulhi((uint32_t)item, a.sweep_mul) + (uint32_t)item) >> a.sweep_shift);
+}
+inline void flow_sweep_divisor(uint32_t d, uint32_t &mul, uint32_t &shift) {
+    uint32_t l = 0;
+    while ((1ull << l) < d) l++;
+    mul = (uint32_t)(((1ull << 32) * ((1ull << l) - d)) / d + 1);
+    shift = l;
 }
 
 __device__ __forceinline__ int ld_relaxed(const int *p) {
@@ -144,6 +188,9 @@ __device__ __forceinline__ int spin_until(const int *flag, int need) {
 }
 
 // Bulk runs of one tile (LOAD: global -> stage, else stage -> global); lane j: edge j.
+// RT: the edge-message type (float, or __half for 16-bit messages: the R run of edge j
+// then fills the first half of its stage slot, so the stage layout does not change).
+template <typename RT>
 __device__ __forceinline__ void flow_runs(const FlowArgs &a, const FlowHdr &h, const uint2 *etab, int KT, int D,
                                           float *stage, uint64_t *bar, bool load, uint64_t pol_keep,
                                           uint64_t pol_stream) {
@@ -151,7 +198,7 @@ __device__ __forceinline__ void flow_runs(const FlowArgs &a, const FlowHdr &h, c
     const int W = 1 << a.lw, z = a.z;
     const int KTW = KT * W;
     float *Lg = reinterpret_cast<float *>(a.L) + (((size_t)h.g * a.n) << a.lw);
-    float *Rg = reinterpret_cast<float *>(a.R) + ((((size_t)h.g * a.E + h.edge_off) * z + h.k0) << a.lw);
+    RT *Rg = reinterpret_cast<RT *>(a.R) + ((((size_t)h.g * a.E + h.edge_off) * z + h.k0) << a.lw);
     for (int j = lane; j < h.d; j += 32) {
         const uint32_t ex = etab[h.edge_off + j].x;
         const int col = ex & 0x7fff, shift = ex >> 16;
@@ -164,14 +211,14 @@ __device__ __forceinline__ void flow_runs(const FlowArgs &a, const FlowHdr &h, c
         const int len1 = min(h.kt, z - p0);
         const uint32_t b1 = (uint32_t)len1 * W * 4;
         const uint32_t b2 = (uint32_t)(h.kt - len1) * W * 4;
-        const uint32_t br = (uint32_t)h.kt * W * 4;
+        const uint32_t br = (uint32_t)h.kt * W * (uint32_t)sizeof(RT);
         const uint64_t pl = reused ? pol_keep : pol_stream;
         const size_t vb = (size_t)col * z;
         float *lg1 = Lg + ((vb + p0) << a.lw);
         float *lg2 = Lg + (vb << a.lw);
-        float *rg = Rg + ((size_t)j * z << a.lw);
+        RT *rg = Rg + ((size_t)j * z << a.lw);
         float *ls = stage + (size_t)j * KTW;
-        float *rs = stage + (size_t)(D + j) * KTW;
+        RT *rs = reinterpret_cast<RT *>(stage + (size_t)(D + j) * KTW);
         if (load) {
             bulk_load(ls, lg1, b1, bar, pl);
             if (b2) bulk_load(ls + (size_t)len1 * W, lg2, b2, bar, pl);
@@ -199,19 +246,67 @@ __device__ __forceinline__ uint32_t flow_deferred_mask(const FlowArgs &a, const 
     return m;
 }
 
+// V consecutive edge messages of one check <-> registers (FP32 or FP16 in the stage).
+template <int V>
+__device__ __forceinline__ void msg_load(const float *p, float (&r)[V]) {
+    *reinterpret_cast<typename Vec<float, V>::type *>(r) = *reinterpret_cast<const typename Vec<float, V>::type *>(p);
+}
+template <int V>
+__device__ __forceinline__ void msg_load(const __half *p, float (&r)[V]) {
+    if constexpr (V == 1) {
+        r[0] = __half2float(*p);
+    } else {
+        __half2 h[V / 2];
+        if constexpr (V == 4)
+            *reinterpret_cast<uint2 *>(h) = *reinterpret_cast<const uint2 *>(p);
+        else
+            *reinterpret_cast<uint32_t *>(h) = *reinterpret_cast<const uint32_t *>(p);
+#pragma unroll
+        for (int i = 0; i < V / 2; i++) {
+            const float2 f = __half22float2(h[i]);
+            r[2 * i] = f.x;
+            r[2 * i + 1] = f.y;
+        }
+    }
+}
+template <int V>
+__device__ __forceinline__ void msg_store(float *p, const float (&r)[V]) {
+    *reinterpret_cast<typename Vec<float, V>::type *>(p) = *reinterpret_cast<const typename Vec<float, V>::type *>(r);
+}
+template <int V>
+__device__ __forceinline__ void msg_store(__half *p, const float (&r)[V]) {  // r already FP16 values: exact
+    if constexpr (V == 1) {
+        *p = __float2half_rn(r[0]);
+    } else {
+        __half2 h[V / 2];
+#pragma unroll
+        for (int i = 0; i < V / 2; i++) h[i] = __floats2half2_rn(r[2 * i], r[2 * i + 1]);
+        if constexpr (V == 4)
+            *reinterpret_cast<uint2 *>(p) = *reinterpret_cast<const uint2 *>(h);
+        else
+            *reinterpret_cast<uint32_t *>(p) = *reinterpret_cast<const uint32_t *>(h);
+    }
+}
+// consumer-warp barrier (named barrier 1): the FP16 generic path reuses R slots as FP32
+// scratch, whose bytes overlap other threads' FP16 messages
+__device__ __forceinline__ void consumers_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kFlowConsumers * 32) : "memory");
+}
+
 // One consumer thread: check (ci) of the tile for V lanes, in place in the stage.
-template <int V, int D, bool HAS_SYN>
+template <int V, int D, bool HAS_SYN, typename RT>
 __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
                                              const uint2 *etab) {
     const int W = 1 << a.lw;
-    const int KT = flow_KT(h.cls, W);
+    const int KT = flow_kt(h.cls, W, a.lw);
     const int KTW = KT * W;
-    const int lanes_v = W / V;
-    const int ci = ct / lanes_v;
-    const int w0 = (ct - ci * lanes_v) * V;
+    const int lv_log2 = a.lw - flow_ilog2(V);  // W / V lanes per check (W >= V)
+    const int ci = ct >> lv_log2;
+    const int w0 = (ct - (ci << lv_log2)) * V;
     if (ci >= h.kt) return;
     const int off = ci * W + w0;
     const float clip = (float)a.clip;
+    constexpr bool H = sizeof(RT) == 2;
     using VT = typename Vec<float, V>::type;
     float q[D][V], ph[D][V];
     int par[V];
@@ -235,7 +330,7 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
 #pragma unroll
                 for (int v = 0; v < V; v++) q[j][v] = lv[v];
             } else {
-                *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+                msg_load<V>(reinterpret_cast<const RT *>(stage + (size_t)(D + j) * KTW) + off, rv);
                 if (fresh_lanes) {  // frame pool: lanes that just took a new frame have r_old = 0
 #pragma unroll
                     for (int v = 0; v < V; v++)
@@ -253,10 +348,10 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
         uint32_t sb[V];
 #pragma unroll
         for (int v = 0; v < V; v++) sb[v] = (uint32_t)par[v] << 31;
-        check_update_f32_d4<V>(reinterpret_cast<float(&)[4][V]>(q), reinterpret_cast<float(&)[4][V]>(ph), sb,
-                               (float)a.mag_max, clip);
+        check_update_f32_d4<V, H>(reinterpret_cast<float(&)[4][V]>(q), reinterpret_cast<float(&)[4][V]>(ph), sb,
+                                  (float)a.mag_max, clip);
     } else {
-        check_update_f32<V, D>(q, ph, par, h.d, (float)a.mag_max, clip);
+        check_update_f32<V, D, H>(q, ph, par, h.d, (float)a.mag_max, clip);
     }
 #pragma unroll
     for (int j = 0; j < D; j++) {
@@ -265,7 +360,7 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
 #pragma unroll
                 for (int v = 0; v < V; v++) q[j][v] = clampT(q[j][v] - ph[j][v], clip);
             }
-            *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(ph[j]);
+            msg_store<V>(reinterpret_cast<RT *>(stage + (size_t)(D + j) * KTW) + off, ph[j]);
             *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(q[j]);
         }
     }
@@ -275,17 +370,21 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
 // exclusive prefix (S, D) pairs stashed in the tile's own shared-memory slots of each edge
 // (free once the edge's L and R are in registers) instead of registers, so the 80-register
 // budget of two resident CTAs per SM holds without spills.  Same arithmetic, in the same
-// order, as check_update_f32.
-template <int V, int D, bool HAS_SYN>
+// order, as check_update_f32.  With FP16 messages the FP32 stash overlaps other threads'
+// FP16 R values, so all consumers read their inputs before the first stash write and keep
+// the new messages in registers until every thread has read its stash back.
+template <int V, int D, bool HAS_SYN, typename RT>
 __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
                                                  const uint2 *etab) {
+    constexpr bool H = sizeof(RT) == 2;
     const int W = 1 << a.lw;
-    const int KT = flow_KT(h.cls, W);
+    const int KT = flow_kt(h.cls, W, a.lw);
     const int KTW = KT * W;
-    const int lanes_v = W / V;
-    const int ci = ct / lanes_v;
-    const int w0 = (ct - ci * lanes_v) * V;
-    if (ci >= h.kt) return;
+    const int lv_log2 = a.lw - flow_ilog2(V);  // W / V lanes per check (W >= V)
+    const int ci = ct >> lv_log2;
+    const int w0 = (ct - (ci << lv_log2)) * V;
+    const bool act = ci < h.kt;
+    if (!H && !act) return;
     const int off = ci * W + w0;
     const float clip = (float)a.clip, mag_max = (float)a.mag_max;
     using VT = typename Vec<float, V>::type;
@@ -294,7 +393,7 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
     const uint32_t fresh_lanes = a.fresh ? a.fresh[h.g] : 0u;
     const uint32_t dmask = flow_deferred_mask(a, h, etab);
     const bool last = h.t == a.defer_last;
-    if (HAS_SYN) {
+    if (HAS_SYN && act) {
         const uint8_t *sp = a.syn + ((((int64_t)h.g * a.S + h.slot) * a.z + h.k0 + ci) << a.lw) + w0;
 #pragma unroll
         for (int v = 0; v < V; v++) par[v] = sp[v] & 1;
@@ -309,10 +408,10 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
             q[j][v] = 0.0f;
             t[j][v] = 0.0f;
         }
-        if (j < h.d) {
+        if (j < h.d && act) {
             float lv[V], rv[V];
             *reinterpret_cast<VT *>(lv) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
-            *reinterpret_cast<VT *>(rv) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+            msg_load<V>(reinterpret_cast<const RT *>(stage + (size_t)(D + j) * KTW) + off, rv);
             const bool dj = (dmask >> j) & 1;  // the L slot already holds q
 #pragma unroll
             for (int v = 0; v < V; v++) {
@@ -323,8 +422,9 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
             }
         }
     }
-    // exclusive prefix (S, D) pairs -> the edge's L / R slots
-    {
+    if (H) consumers_sync();
+    if (act) {
+        // exclusive prefix (S, D) pairs -> the edge's L / R slots
         float ps[V], pd[V];
 #pragma unroll
         for (int v = 0; v < V; v++) {
@@ -344,32 +444,45 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
                 }
             }
         }
-    }
-    float ss[V], sd[V];
+        float ss[V], sd[V];
 #pragma unroll
-    for (int v = 0; v < V; v++) {
-        ss[v] = 1.0f;
-        sd[v] = 0.0f;
-    }
+        for (int v = 0; v < V; v++) {
+            ss[v] = 1.0f;
+            sd[v] = 0.0f;
+        }
 #pragma unroll
-    for (int j = D - 1; j >= 0; j--) {
-        if (j < h.d) {
-            float xs[V], xd[V], rr[V], ll[V];
-            *reinterpret_cast<VT *>(xs) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
-            *reinterpret_cast<VT *>(xd) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
+        for (int j = D - 1; j >= 0; j--) {
+            if (j < h.d) {
+                float xs[V], xd[V], rr[V], ll[V];
+                *reinterpret_cast<VT *>(xs) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
+                *reinterpret_cast<VT *>(xd) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
 #pragma unroll
-            for (int v = 0; v < V; v++) {
-                const float S = fmaf(xs[v], ss[v], xd[v] * sd[v]), Dv = fmaf(xs[v], sd[v], xd[v] * ss[v]);
-                const float mag = sd_mag(S, Dv, mag_max);
-                rr[v] = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
-                ll[v] = clampT(q[j][v] + rr[v], clip);
-                if (((dmask >> j) & 1) && !last) ll[v] = clampT(ll[v] - rr[v], clip);  // deferred: next q
-                const float ns = fmaf(t[j][v], sd[v], ss[v]);
-                sd[v] = fmaf(t[j][v], ss[v], sd[v]);
-                ss[v] = ns;
+                for (int v = 0; v < V; v++) {
+                    const float S = fmaf(xs[v], ss[v], xd[v] * sd[v]), Dv = fmaf(xs[v], sd[v], xd[v] * ss[v]);
+                    const float mag = msg_round<H>(sd_mag(S, Dv, mag_max));
+                    rr[v] = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
+                    ll[v] = clampT(q[j][v] + rr[v], clip);
+                    if (((dmask >> j) & 1) && !last) ll[v] = clampT(ll[v] - rr[v], clip);  // deferred: next q
+                    const float ns = fmaf(t[j][v], sd[v], ss[v]);
+                    sd[v] = fmaf(t[j][v], ss[v], sd[v]);
+                    ss[v] = ns;
+                }
+                if (H) {  // the R slot may still hold another thread's stash: r waits in q[j]
+#pragma unroll
+                    for (int v = 0; v < V; v++) q[j][v] = rr[v];
+                } else {
+                    *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(rr);
+                }
+                *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(ll);
             }
-            *reinterpret_cast<VT *>(stage + (size_t)(D + j) * KTW + off) = *reinterpret_cast<VT *>(rr);
-            *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(ll);
+        }
+    }
+    if (H) {
+        consumers_sync();
+        if (act) {
+#pragma unroll
+            for (int j = 0; j < D; j++)
+                if (j < h.d) msg_store<V>(reinterpret_cast<RT *>(stage + (size_t)(D + j) * KTW) + off, q[j]);
         }
     }
 }
@@ -381,7 +494,7 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
         tc = c_;                              \
     }
 
-template <bool HAS_SYN, bool PROF>
+template <bool HAS_SYN, bool PROF, typename RT = float>
 __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(FlowArgs a) {
     if (a.n_active && *(volatile const int *)a.n_active == 0) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -425,11 +538,16 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         // they are larger than the item in hand.  Resolved headers go to the loader warp
         // through a small queue, so dependency polling overlaps the bulk-copy issue.
         int n2 = 0;
-        if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
-        int n1 = __shfl_sync(0xffffffffu, n2, 0);
+        if (lane == 0) n2 = atomicAdd(a.counter, 1);
+        auto next_claim = [&]() {
+            const int n = __shfl_sync(0xffffffffu, n2, 0);
+            if (n < a.item_end && lane == 0) n2 = atomicAdd(a.counter, 1);
+            return n;
+        };
+        auto record = [&](int n) { return __ldg(a.items + (n - flow_sweep_of(a, n) * a.sweep_items)); };
+        int n1 = next_claim();
         int2 r1 = make_int2(0, 0);
-        if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
-        if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
+        if (n1 < a.item_end) r1 = record(n1);
         int sentinels = 0;
         unsigned long long n_waited = 0, n_polls = 0, n_tiles = 0;
         // lane j < d: the flags of the previous writer of edge j's column covering this
@@ -441,25 +559,25 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             need = h.t + 1 - (int)((dy >> 15) & 1);
             if (need <= 0) return;
             const uint2 pst = stab[dy & 0x7fff];
-            const int KTp = flow_KT(pst.x >> 24, W);
-            fl = a.flags + (size_t)h.g * a.nkb_total + pst.y;
+            const int pcls = pst.x >> 24;
+            fl = a.flags + ((size_t)h.g * a.nkb_total + pst.y) * QCL_FLAG_STRIDE;
             int a0 = h.k0 + (int)(dy >> 16);
             a0 -= (a0 >= a.z) ? a.z : 0;
             const int b = a0 + h.kt - 1;
-            lo = a0 / KTp;
-            nlo = min(b, a.z - 1) / KTp - lo + 1;
-            nfl = nlo + (b >= a.z ? (b - a.z) / KTp + 1 : 0);
+            lo = flow_kb_of(a0, pcls, W, a.lw);
+            nlo = flow_kb_of(min(b, a.z - 1), pcls, W, a.lw) - lo + 1;
+            nfl = nlo + (b >= a.z ? flow_kb_of(b - a.z, pcls, W, a.lw) + 1 : 0);
         };
         auto resolve = [&](int item, int2 e) {
             FlowHdr h;
-            h.t = a.t_base + item / a.sweep_items;
+            h.t = a.t_base + flow_sweep_of(a, item);
             h.slot = e.x & 0xffff;
             h.g = e.x >> 16;
             const uint2 st = stab[h.slot];
             h.edge_off = st.x & 0xffff;
             h.d = (st.x >> 16) & 0xff;
             h.cls = st.x >> 24;
-            const int KT = flow_KT(h.cls, W);
+            const int KT = flow_kt(h.cls, W, a.lw);
             h.k0 = e.y * KT;
             h.kt = min(KT, a.z - h.k0);
             return h;
@@ -478,16 +596,15 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 }
                 if (++sentinels == kFlowStorers) break;
             } else {
-                n1 = __shfl_sync(0xffffffffu, n2, 0);
-                if (n1 < a.item_end) r1 = __ldg(a.items + (n1 % a.sweep_items));
-                if (lane == 0) n2 = a.item_begin + atomicAdd(a.counter, 1);
+                n1 = next_claim();
+                if (n1 < a.item_end) r1 = record(n1);
                 FLOW_TICK(1);
                 const FlowHdr h = resolve(item, e);
                 if (a.gactive && !a.gactive[h.g]) {
                     // every frame of this lane group has converged: its outputs are frozen,
                     // so the tile is not updated -- only released for the group's later tiles
                     __syncwarp();
-                    if (lane == 0) st_release(a.flags + (size_t)h.g * a.nkb_total + stab[h.slot].y + e.y, h.t + 1);
+                    if (lane == 0) st_release(a.flags + ((size_t)h.g * a.nkb_total + stab[h.slot].y + e.y) * QCL_FLAG_STRIDE, h.t + 1);
                     goto next_item;
                 }
                 // wait for the previous writers of every column of this tile: all covering
@@ -499,11 +616,11 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                     flag_plan(h, fl, need, lo, nlo, nfl);
 #pragma unroll
                     for (int m = 0; m < 4; m++)
-                        if (m < nfl) fv[m] = ld_relaxed(fl + (m < nlo ? lo + m : m - nlo));
+                        if (m < nfl) fv[m] = ld_relaxed(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE);
 #pragma unroll
                     for (int m = 0; m < 4; m++)
-                        if (m < nfl && fv[m] < need) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo), need);
-                    for (int m = 4; m < nfl; m++) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo), need);
+                        if (m < nfl && fv[m] < need) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need);
+                    for (int m = 4; m < nfl; m++) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need);
                 }
                 FLOW_TICK(2);
                 if (prof) {
@@ -541,8 +658,11 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         const uint64_t pol_stream = policy_evict_first();
         const uint64_t pol_keep = policy_evict_last();
         int sentinels = 0;
+        const bool lprof = PROF;
         for (int it = 0, s = 0, ph = 0, q = 0, qph = 0;; it++) {
+            if (lprof) tc = clock64();
             mbar_wait_sleep(&ready[q], qph);
+            if (lprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
             const FlowHdr h = hq[q];
             __syncwarp();
             if (lane == 0) mbar_arrive(&qfree[q]);
@@ -551,6 +671,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 qph ^= 1;
             }
             if (it >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
+            if (lprof) { const long long c_ = clock64(); acc[1] += c_ - tc; tc = c_; }
             if (h.kt < 0) {
                 if (lane == 0) {
                     hdr[s].kt = -1;
@@ -559,21 +680,28 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 if (++sentinels == kFlowStorers) break;
             } else {
                 fence_proxy_async_global();  // observed flags -> ordered before the bulk (async proxy) reads
-                const int KT = flow_KT(h.cls, W);
+                const int KT = flow_kt(h.cls, W, a.lw);
                 // runs moved: d L runs, plus the R runs of edges not under degree-1 deferral
                 const uint32_t nr = (uint32_t)h.d - __popc(flow_deferred_mask(a, h, etab));
                 if (lane == 0) {
                     hdr[s] = h;
-                    mbar_arrive_expect_tx(&full[s], ((uint32_t)h.d + nr) * (uint32_t)(h.kt * W * 4));
+                    mbar_arrive_expect_tx(&full[s], ((uint32_t)h.d * 4 + nr * (uint32_t)sizeof(RT)) * (uint32_t)(h.kt * W));
                 }
                 __syncwarp();
-                flow_runs(a, h, etab, KT, flow_class_D(h.cls), stages + (size_t)s * kStageElems, &full[s], true,
+                flow_runs<RT>(a, h, etab, KT, flow_class_D(h.cls), stages + (size_t)s * kStageElems, &full[s], true,
                           pol_keep, pol_stream);
+                __syncwarp();
+                if (lprof) acc[2] += clock64() - tc;
             }
             if (++s == S) {
                 s = 0;
                 ph ^= 1;
             }
+        }
+        if (lprof && lane == 0) {
+            atomicAdd(a.stats + 7, (unsigned long long)acc[1]);
+            atomicAdd(a.stats + 8, (unsigned long long)acc[2]);
+            atomicAdd(a.stats + 15, (unsigned long long)acc[0]);
         }
         return;
     }
@@ -592,8 +720,8 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             if (sprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
             const FlowHdr h = hdr[s];
             if (h.kt < 0) break;
-            const int KT = flow_KT(h.cls, W);
-            flow_runs(a, h, etab, KT, flow_class_D(h.cls), stages + (size_t)s * kStageElems, nullptr, false,
+            const int KT = flow_kt(h.cls, W, a.lw);
+            flow_runs<RT>(a, h, etab, KT, flow_class_D(h.cls), stages + (size_t)s * kStageElems, nullptr, false,
                       pol_keep, pol_stream);
             bulk_commit();
             if (sprof) { const long long c_ = clock64(); acc[1] += c_ - tc; tc = c_; }
@@ -605,7 +733,8 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             fence_proxy_async_global();
             __syncwarp();
             if (lane == 0) {  // ... before the tile is released to its dependents
-st_release(a.flags + (size_t)h.g * a.nkb_total + stab[h.slot].y + h.k0 / KT, h.t + 1);
+                st_release(a.flags + ((size_t)h.g * a.nkb_total + stab[h.slot].y + flow_kb_of(h.k0, h.cls, W, a.lw)) * QCL_FLAG_STRIDE,
+                           h.t + 1);
             }
             if (sprof) acc[3] += clock64() - tc;
         }
@@ -629,11 +758,11 @@ st_release(a.flags + (size_t)h.g * a.nkb_total + stab[h.slot].y + h.k0 / KT, h.t
         } else {
             float *stage = stages + (size_t)s * kStageElems;
             if (h.cls == 0)
-                flow_consume<flow_class_V(0), 4, HAS_SYN>(a, h, stage, ct, etab);
+                flow_consume<flow_class_V(0), 4, HAS_SYN, RT>(a, h, stage, ct, etab);
             else if (h.cls == 1)
-                flow_consume_gen<flow_class_V(1), 8, HAS_SYN>(a, h, stage, ct, etab);
+                flow_consume_gen<flow_class_V(1), 8, HAS_SYN, RT>(a, h, stage, ct, etab);
             else
-                flow_consume_gen<flow_class_V(2), 12, HAS_SYN>(a, h, stage, ct, etab);
+                flow_consume_gen<flow_class_V(2), 12, HAS_SYN, RT>(a, h, stage, ct, etab);
             fence_proxy_async_smem();  // this thread's STS -> visible to the bulk-store engine
             __syncwarp();
             if (lane == 0) mbar_arrive(&done[s]);

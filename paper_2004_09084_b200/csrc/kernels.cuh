@@ -13,6 +13,8 @@
 // in k) and one contiguous run of R: every access is a coalesced V*sizeof(T)-wide
 // vector access and each algorithmic byte crosses the memory system once.
 #pragma once
+#include <cuda_fp16.h>
+
 #include <cstdint>
 
 #include "phi.cuh"
@@ -232,10 +234,19 @@ __device__ __forceinline__ float sd_mag(float S, float D, float mag_max) {
     return fminf(lg2_approx(S * rcp_approx(D)) * 0.6931471805599453f, mag_max);
 }
 
+// 16-bit edge messages (QCL_PREC_FP32_MSG16): |r| rounded to FP16 before it is used, so
+// the posterior update and the message store see the same value and the next sweep's
+// q = L - r_old subtracts exactly what was added
+template <bool H>
+__device__ __forceinline__ float msg_round(float mag) {
+    if constexpr (H) return __half2float(__float2half_rn(mag));
+    return mag;
+}
+
 // Any degree <= D (edges j >= d are neutral: t = 0, the identity (1, 0) of the combine):
 //   in:  q[j][v] = clip(L - r_old), par[v] = syndrome bit
 //   out: q[j][v] <- new posterior clip(q + r), ph[j][v] <- new message r
-template <int V, int D>
+template <int V, int D, bool H = false>
 __device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D][V], int (&par)[V], int d,
                                                  float mag_max, float clip) {
 #pragma unroll
@@ -264,7 +275,7 @@ __device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D
         for (int j = D - 1; j >= 0; j--) {
             if (j < d) {
                 const float S = fmaf(xs[j], ss, xd[j] * sd), Dv = fmaf(xs[j], sd, xd[j] * ss);
-                const float mag = sd_mag(S, Dv, mag_max);
+                const float mag = msg_round<H>(sd_mag(S, Dv, mag_max));
                 const float r = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
                 ph[j][v] = r;
                 q[j][v] = clampT(q[j][v] + r, clip);
@@ -282,7 +293,7 @@ __device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D
 // because the FP32 state never holds -0.0 (reset/upload canonicalise it; r != -0.0 and,
 // under round-to-nearest, q + r and L - r_old are -0.0 only for -0.0 operands), so the
 // sign bit == (q < 0).  Lane pairs use the packed FP32 instructions (FFMA2/FADD2/FMUL2).
-template <int V>
+template <int V, bool H = false>
 __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph)[4][V], const uint32_t (&synbit)[V],
                                                     float mag_max, float clip) {
 #pragma unroll
@@ -308,7 +319,7 @@ __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph
         Dv[3] = fmaf(t[2], S01, D01);
 #pragma unroll
         for (int j = 0; j < 4; j++) {
-            const float mag = sd_mag(S[j], Dv[j], mag_max);
+            const float mag = msg_round<H>(sd_mag(S[j], Dv[j], mag_max));
             const float r = __uint_as_float(__float_as_uint(mag) | (qs[j] ^ par));
             ph[j][v] = r;
             q[j][v] = clampT(q[j][v] + r, clip);
@@ -631,9 +642,9 @@ __global__ void reset_kernel(const T *llr, T *L, int64_t count, double clip) {
 }
 
 // Reference-layout FP64 state <-> lanes.  post (B, n); msg (B, E*z) [e][k].
-template <typename T>
+template <typename T, typename RT = T>
 __global__ void state_in_kernel(const double *post, const double *msg, int64_t B, int64_t n, int64_t Ez,
-                                int lw, T *L, T *R, int64_t Bp) {
+                                int lw, T *L, RT *R, int64_t Bp) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int W = 1 << lw;
     int64_t w = i & (W - 1), rest = i >> lw;
@@ -643,11 +654,17 @@ __global__ void state_in_kernel(const double *post, const double *msg, int64_t B
     }
     if (i < Bp * Ez) {
         int64_t x = rest % Ez, g = rest / Ez, b = (g << lw) + w;
-        R[i] = (b < B && msg) ? (T)msg[b * Ez + x] + (T)0 : (T)0;
+        if constexpr (sizeof(RT) == 2)  // one rounding, double -> FP16
+            R[i] = __double2half((b < B && msg) ? msg[b * Ez + x] + 0.0 : 0.0);
+        else
+            R[i] = (b < B && msg) ? (T)msg[b * Ez + x] + (T)0 : (T)0;
     }
 }
-template <typename T>
-__global__ void state_out_kernel(const T *L, const T *R, int64_t B, int64_t n, int64_t Ez, int lw,
+__device__ __forceinline__ double msg_f64(double x) { return x; }
+__device__ __forceinline__ double msg_f64(float x) { return (double)x; }
+__device__ __forceinline__ double msg_f64(__half x) { return (double)__half2float(x); }
+template <typename T, typename RT = T>
+__global__ void state_out_kernel(const T *L, const RT *R, int64_t B, int64_t n, int64_t Ez, int lw,
                                  double *post, double *msg) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // over B * max(n, Ez), row-major
     int64_t b = i / (n > Ez ? n : Ez), x = i % (n > Ez ? n : Ez);
@@ -655,7 +672,7 @@ __global__ void state_out_kernel(const T *L, const T *R, int64_t B, int64_t n, i
     const int W = 1 << lw;
     int64_t g = b >> lw, w = b & (W - 1);
     if (post && x < n) post[b * n + x] = (double)L[((g * n + x) << lw) + w];
-    if (msg && x < Ez) msg[b * Ez + x] = (double)R[((g * Ez + x) << lw) + w];
+    if (msg && x < Ez) msg[b * Ez + x] = msg_f64(R[((g * Ez + x) << lw) + w]);
 }
 
 // Target syndrome (B, m) in original row order -> u8[G][S][z][W] in slot order.

@@ -85,7 +85,9 @@ struct qcl_state {
     cudaEvent_t fork = nullptr, join[kSideStreams] = {};
     int64_t B = 0, Bp = 0;
     int prec = QCL_PREC_FP32, lw = 0, W = 1, G = 1;
-    size_t esz = 4;
+    int api_prec = QCL_PREC_FP32;  // as created; prec is the posterior type (FP32 for MSG16)
+    bool msg16 = false;            // FP16 edge messages (QCL_PREC_FP32_MSG16, flow engine only)
+    size_t esz = 4, resz = 4;      // posterior / edge-message element sizes
     cudaStream_t stream = nullptr;
     void *llr = nullptr, *L = nullptr, *R = nullptr;
     uint8_t *syn = nullptr;  // lanes layout, valid if has_syn
@@ -413,6 +415,12 @@ static bool use_flow(const qcl_state *st) {
            st->W >= 4 && st->f_grid >= 0;
 }
 
+// FP16 edge messages exist only in the flow kernel's message path.
+static int msg16_unsupported(const qcl_state *st, const char *what) {
+    return fail(QCL_EUNSUP, "16-bit edge messages (QCL_PREC_FP32_MSG16) run on the flow engine only: %s "
+                "(engine %d, max row degree %d, %d lanes)", what, st->engine, st->plan->max_degree, st->W);
+}
+
 // Tiling (per slot), the item list of one sweep and the flag/counter buffers.
 static int ensure_flow(qcl_state *st, int counters) {
     const qcl_plan *p = st->plan;
@@ -441,7 +449,7 @@ static int ensure_flow(qcl_state *st, int counters) {
         CK(cudaMemcpy(st->fslot_tab, stab.data(), sizeof(uint2) * p->S, cudaMemcpyHostToDevice));
         CK(cudaMalloc(&st->fitems, sizeof(int2) * items.size()));
         CK(cudaMemcpy(st->fitems, items.data(), sizeof(int2) * items.size(), cudaMemcpyHostToDevice));
-        CK(cudaMalloc(&st->fflags, sizeof(int) * (size_t)st->G * st->f_nkb_total));
+        CK(cudaMalloc(&st->fflags, sizeof(int) * QCL_FLAG_STRIDE * (size_t)st->G * st->f_nkb_total));
         if (env_int("QCL_FLOW_STATS", 0)) {
             CK(cudaMalloc(&st->fstats, 16 * sizeof(unsigned long long)));
             CK(cudaMemset(st->fstats, 0, 16 * sizeof(unsigned long long)));
@@ -465,7 +473,8 @@ static int ensure_flow(qcl_state *st, int counters) {
         }
         st->f_stages = stages;
         for (auto kern : {flow_kernel<false, false>, flow_kernel<true, false>, flow_kernel<false, true>,
-                          flow_kernel<true, true>})
+                          flow_kernel<true, true>, flow_kernel<false, false, __half>, flow_kernel<true, false, __half>,
+                          flow_kernel<false, true, __half>, flow_kernel<true, true, __half>})
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<false, false>, kFlowThreads, smem));
         st->f_grid = sms * std::max(1, per_sm);
@@ -490,7 +499,7 @@ static int flow_defer_last(int max_iterations) {
 static int enqueue_flow_reset(qcl_state *st, int counters) {
     int rc = ensure_flow(st, counters);
     if (rc) return rc;
-    CK(cudaMemsetAsync(st->fflags, 0, sizeof(int) * (size_t)st->G * st->f_nkb_total, st->stream));
+    CK(cudaMemsetAsync(st->fflags, 0, sizeof(int) * QCL_FLAG_STRIDE * (size_t)st->G * st->f_nkb_total, st->stream));
     CK(cudaMemsetAsync(st->fcounters, 0, sizeof(int) * counters, st->stream));
     return QCL_OK;
 }
@@ -504,7 +513,7 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.edge_tab = p->fedge_tab;
     a.items = st->fitems;
     a.sweep_items = (int32_t)st->f_sweep_items;
-    a.item_begin = 0;
+    flow_sweep_divisor((uint32_t)st->f_sweep_items, a.sweep_mul, a.sweep_shift);
     a.item_end = (int32_t)(T * st->f_sweep_items);
     a.t_base = t0;
     a.counter = st->fcounters + counter;
@@ -529,12 +538,16 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.eps = eps;
     a.mag_max = mag_bound(clip, eps);
     const size_t smem = flow_smem_bytes(p->S, p->E, st->f_stages);
-    const int64_t grid = std::min<int64_t>(st->f_grid, a.item_end - a.item_begin);
+    const int64_t grid = std::min<int64_t>(st->f_grid, a.item_end);
     const bool prof = st->fstats != nullptr;
-    if (st->has_syn)
-        (prof ? flow_kernel<true, true> : flow_kernel<true, false>)<<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
+    void (*kern)(FlowArgs);
+    if (st->msg16)
+        kern = st->has_syn ? (prof ? flow_kernel<true, true, __half> : flow_kernel<true, false, __half>)
+                           : (prof ? flow_kernel<false, true, __half> : flow_kernel<false, false, __half>);
     else
-        (prof ? flow_kernel<false, true> : flow_kernel<false, false>)<<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
+        kern = st->has_syn ? (prof ? flow_kernel<true, true> : flow_kernel<true, false>)
+                           : (prof ? flow_kernel<false, true> : flow_kernel<false, false>);
+    kern<<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
     CK(cudaGetLastError());
     st->launches_layer++;
     st->launches_all++;
@@ -846,15 +859,19 @@ static int lanes_log2(int64_t B) {
 int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **out) {
     if (!p || !out) return fail(QCL_EVALUE, "NULL argument");
     if (batch < 1) return fail(QCL_EVALUE, "batch must be at least 1");
-    if (precision != QCL_PREC_FP32 && precision != QCL_PREC_FP64)
+    if (precision != QCL_PREC_FP32 && precision != QCL_PREC_FP64 && precision != QCL_PREC_FP32_MSG16)
         return fail(QCL_EVALUE, "unknown precision %d", precision);
     CK(cudaSetDevice(p->device));
     auto st = new qcl_state();
     st->plan = p;
     st->B = batch;
-    st->prec = precision;
-    st->esz = precision == QCL_PREC_FP32 ? 4 : 8;
-    st->lw = lanes_log2(batch);
+    st->api_prec = precision;
+    st->msg16 = precision == QCL_PREC_FP32_MSG16;
+    st->prec = st->msg16 ? QCL_PREC_FP32 : precision;
+    st->esz = st->prec == QCL_PREC_FP32 ? 4 : 8;
+    st->resz = st->msg16 ? 2 : st->esz;
+    // FP16 runs of W lanes must stay whole 16-byte bulk-copy units: at least 8 lanes
+    st->lw = st->msg16 ? std::max(3, lanes_log2(batch)) : lanes_log2(batch);
     st->W = 1 << st->lw;
     st->G = (int)cdiv(batch, st->W);
     st->Bp = (int64_t)st->G * st->W;
@@ -874,7 +891,7 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
     };
     al(&st->llr, nl * st->esz);
     al(&st->L, nl * st->esz);
-    al(&st->R, ne * st->esz);
+    al(&st->R, ne * st->resz);
     al((void **)&st->syn, nm);
     al((void **)&st->words, (size_t)batch * p->n);
     al((void **)&st->conv, st->Bp);
@@ -914,9 +931,9 @@ int qcl_state_destroy(qcl_state *st) {
         const double T = h[2] ? (double)h[2] : 1.0;
         fprintf(stderr, "[flow stats] cycles/tile scheduler: qfree %.0f claim %.0f deps %.0f queue %.0f | consumer: "
                         "full-wait %.0f compute %.0f | storer(x2 tiles): done-wait %.0f issue %.0f read %.0f "
-                        "write+release %.0f\n",
+                        "write+release %.0f | loader: ready-wait %.0f empty-wait %.0f issue %.0f\n",
                 h[3] / T, h[4] / T, h[5] / T, h[6] / T, h[9] / T, h[10] / T, 2 * h[11] / T, 2 * h[12] / T,
-                2 * h[13] / T, 2 * h[14] / T);
+                2 * h[13] / T, 2 * h[14] / T, h[15] / T, h[7] / T, h[8] / T);
     }
     if (st->sweep_exec) cudaGraphExecDestroy(st->sweep_exec);
     if (st->decode_exec) cudaGraphExecDestroy(st->decode_exec);
@@ -1069,10 +1086,10 @@ int qcl_state_get_llr(qcl_state *st, double *llr) {
     const int64_t total = st->B * p->n;
     const unsigned grid = (unsigned)cdiv(total, kBlock);
     if (st->prec == QCL_PREC_FP32)
-        state_out_kernel<float><<<grid, kBlock, 0, st->stream>>>((const float *)st->llr, nullptr, st->B, p->n, 0,
+        state_out_kernel<float, float><<<grid, kBlock, 0, st->stream>>>((const float *)st->llr, nullptr, st->B, p->n, 0,
                                                                   st->lw, (double *)st->staging, nullptr);
     else
-        state_out_kernel<double><<<grid, kBlock, 0, st->stream>>>((const double *)st->llr, nullptr, st->B, p->n,
+        state_out_kernel<double, double><<<grid, kBlock, 0, st->stream>>>((const double *)st->llr, nullptr, st->B, p->n,
                                                                    0, st->lw, (double *)st->staging, nullptr);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(llr, st->staging, total * 8, cudaMemcpyDeviceToHost, st->stream));
@@ -1116,7 +1133,7 @@ static int enqueue_reset(qcl_state *st, double clip) {
         reset_kernel<double><<<(unsigned)cdiv(nl, kBlock), kBlock, 0, st->stream>>>((const double *)st->llr,
                                                                                      (double *)st->L, nl, clip);
     CK(cudaGetLastError());
-    CK(cudaMemsetAsync(st->R, 0, (size_t)st->Bp * p->E * p->z * st->esz, st->stream));
+    CK(cudaMemsetAsync(st->R, 0, (size_t)st->Bp * p->E * p->z * st->resz, st->stream));
     st->launches_all++;
     return QCL_OK;
 }
@@ -1141,7 +1158,11 @@ int qcl_state_upload(qcl_state *st, const double *posterior, const double *messa
     if (messages) CK(cudaMemcpyAsync(sm, messages, mb, cudaMemcpyHostToDevice, st->stream));
     const int64_t total = st->Bp * std::max<int64_t>(p->n, Ez);
     const unsigned grid = (unsigned)cdiv(total, kBlock);
-    if (st->prec == QCL_PREC_FP32)
+    if (st->msg16)
+        state_in_kernel<float, __half><<<grid, kBlock, 0, st->stream>>>(sp, messages ? sm : nullptr, st->B, p->n,
+                                                                         Ez, st->lw, (float *)st->L, (__half *)st->R,
+                                                                         st->Bp);
+    else if (st->prec == QCL_PREC_FP32)
         state_in_kernel<float><<<grid, kBlock, 0, st->stream>>>(sp, messages ? sm : nullptr, st->B, p->n, Ez,
                                                                  st->lw, (float *)st->L, (float *)st->R, st->Bp);
     else
@@ -1163,7 +1184,10 @@ int qcl_state_download(qcl_state *st, double *posterior, double *messages) {
     double *sp = (double *)st->staging, *sm = sp + st->B * p->n;
     const int64_t total = st->B * std::max<int64_t>(p->n, Ez);
     const unsigned grid = (unsigned)cdiv(total, kBlock);
-    if (st->prec == QCL_PREC_FP32)
+    if (st->msg16)
+        state_out_kernel<float, __half><<<grid, kBlock, 0, st->stream>>>((const float *)st->L, (const __half *)st->R,
+                                                                          st->B, p->n, Ez, st->lw, sp, sm);
+    else if (st->prec == QCL_PREC_FP32)
         state_out_kernel<float><<<grid, kBlock, 0, st->stream>>>((const float *)st->L, (const float *)st->R, st->B,
                                                                   p->n, Ez, st->lw, sp, sm);
     else
@@ -1182,6 +1206,12 @@ int qcl_state_layers(qcl_state *st, int32_t first, int32_t count, double llr_cli
     if (first < 0 || count < 0 || first + count > p->n_layers)
         return fail(QCL_EVALUE, "layer range [%d, %d) outside [0, %d)", first, first + count, p->n_layers);
     CK(cudaSetDevice(p->device));
+    if (st->msg16) {
+        if (!use_flow(st) || first != 0 || count != p->n_layers) return msg16_unsupported(st, "whole sweeps only");
+        int rc = ensure_flow(st, 1);
+        if (rc) return rc;
+        if (!use_flow(st)) return msg16_unsupported(st, "tables exceed shared memory");
+    }
     const bool saved_et = st->g_et;
     st->g_et = false;  // direct layer launches never skip
     if (use_flow(st) && first == 0 && count == p->n_layers) {
@@ -1234,6 +1264,8 @@ static int validate_cfg(const qcl_config *cfg) {
     if (cfg->max_iterations < 1) return fail(QCL_EVALUE, "max_iterations must be at least 1");
     if (!(cfg->llr_clip > 0)) return fail(QCL_EVALUE, "llr_clip must be positive");
     if (!(cfg->phi_epsilon > 0 && cfg->phi_epsilon < 1)) return fail(QCL_EVALUE, "phi_epsilon must be in (0, 1)");
+    if (cfg->precision != QCL_PREC_FP32 && cfg->precision != QCL_PREC_FP64 && cfg->precision != QCL_PREC_FP32_MSG16)
+        return fail(QCL_EVALUE, "unknown precision %d", cfg->precision);
     return QCL_OK;
 }
 
@@ -1300,7 +1332,7 @@ static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
 static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     int rc = validate_cfg(cfg);
     if (rc) return rc;
-    if (cfg->precision != st->prec) return fail(QCL_EVALUE, "config precision differs from the state's");
+    if (cfg->precision != st->api_prec) return fail(QCL_EVALUE, "config precision differs from the state's");
     const qcl_plan *p = st->plan;
     CK(cudaSetDevice(p->device));
     st->launches_layer = st->launches_all = 0;
@@ -1308,6 +1340,7 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     const bool et = cfg->early_termination != 0;
     if (use_flow(st) && (rc = ensure_flow(st, cfg->max_iterations))) return rc;  // allocations outside capture
     st->flow_decode = use_flow(st) && (int64_t)cfg->max_iterations * st->f_sweep_items + 8LL * st->f_grid < (1LL << 31);
+    if (st->msg16 && !st->flow_decode) return msg16_unsupported(st, "this decode");
     if (!st->profiling && !(sync && et)) {
         const bool stale = !st->decode_exec || st->d_clip != cfg->llr_clip || st->d_eps != cfg->phi_epsilon ||
                            st->d_syn != st->has_syn || st->d_et != et || st->d_iters != cfg->max_iterations ||
@@ -1432,7 +1465,7 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
     if (!st || !conv || !iters || !err) return fail(QCL_EVALUE, "NULL argument");
     int rc = validate_cfg(cfg);
     if (rc) return rc;
-    if (cfg->precision != st->prec) return fail(QCL_EVALUE, "config precision differs from the state's");
+    if (cfg->precision != st->api_prec) return fail(QCL_EVALUE, "config precision differs from the state's");
     if (!cfg->early_termination) return fail(QCL_EVALUE, "the frame pool needs early termination");
     if (n_frames < 1) return fail(QCL_EVALUE, "n_frames must be at least 1");
     if (!(snr > 0)) return fail(QCL_EVALUE, "snr must be positive");
@@ -1479,7 +1512,7 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
     CK(cudaEventRecord(st->ev0, sm));
     if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
     enqueue_group_active(st);
-    CK(cudaMemsetAsync(st->fflags, 0, sizeof(int) * (size_t)st->G * st->f_nkb_total, sm));
+    CK(cudaMemsetAsync(st->fflags, 0, sizeof(int) * QCL_FLAG_STRIDE * (size_t)st->G * st->f_nkb_total, sm));
     st->pool_active = true;
     st->g_et = true;
     const unsigned gb = (unsigned)cdiv(st->Bp, kBlock);
@@ -1606,6 +1639,7 @@ int qcl_state_kernel_stats(qcl_state *st, int64_t *layer_launches, float *layer_
 
 int qcl_state_set_engine(qcl_state *st, int32_t engine) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
+    if (st->msg16 && engine != 4 && engine != 6) return msg16_unsupported(st, "engine switch refused");
     if (engine == 4 || engine == 6) {  // flow engine (persistent dataflow decode); 6: with CUDA events
         st->profiling = engine == 6;
         st->engine = 4;
@@ -1642,7 +1676,7 @@ int qcl_decode(qcl_plan *p, const qcl_config *cfg, const void *llr0, int32_t llr
     {
         std::lock_guard<std::mutex> lk(p->cache_mu);
         for (size_t i = 0; i < p->cache.size(); i++)
-            if (p->cache[i]->B == batch && p->cache[i]->prec == cfg->precision) {
+            if (p->cache[i]->B == batch && p->cache[i]->api_prec == cfg->precision) {
                 st = p->cache[i];
                 p->cache.erase(p->cache.begin() + i);
                 break;

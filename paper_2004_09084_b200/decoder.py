@@ -8,11 +8,15 @@ numeric operation runs in ``libqcldpc_b200.so`` (hand-written sm_100a CUDA behin
 C ABI); this module only validates arguments, moves arrays across the ABI and
 shapes results.
 
-Two precisions, chosen per decoder:
+Three precisions, chosen per decoder:
   * ``precision="fp32"`` (default) -- the performance path: FP32 posteriors and edge
     messages, exclusive Phi-sums, fast Phi (``csrc/phi.cuh``).
   * ``precision="fp64"`` -- the parity path: FP64 state, the reference's own
     ``total - own`` formula and numpy fold order, libdevice log1p/expm1.
+  * ``precision="fp32-msg16"`` -- opt-in, beyond parity: FP32 posteriors, FP16 edge
+    messages (12 instead of 16 bytes per edge and iteration).  Whole decodes and whole
+    sweeps on the flow engine only; its decisions are not bit-identical to ``"fp32"``
+    (FER parity is statistical).
 
 Extra keywords beyond the reference: ``device`` (CUDA ordinal) and ``precision``.
 ``ShardedDecoder`` spreads a batch over several GPUs of one process

@@ -296,6 +296,55 @@ __device__ __forceinline__ void check_update_f32(float (&q)[D][V], float (&ph)[D
 template <int V, bool H = false>
 __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph)[4][V], const uint32_t (&synbit)[V],
                                                     float mag_max, float clip) {
+#ifndef QCL_PACKED_F32X2
+#define QCL_PACKED_F32X2 1
+#endif
+    if constexpr (QCL_PACKED_F32X2 && V % 2 == 0) {
+        // lane pairs on the packed FP32 pipe (FMUL2/FFMA2/FADD2: two IEEE round-to-nearest
+        // results per instruction, the same values as the scalar ops below)
+#pragma unroll
+        for (int v = 0; v < V; v += 2) {
+            uint32_t qs[4][2];
+            float2 t[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                qs[j][0] = __float_as_uint(q[j][v]) & 0x80000000u;
+                qs[j][1] = __float_as_uint(q[j][v + 1]) & 0x80000000u;
+                const float2 e = __fmul2_rn(make_float2(fabsf(q[j][v]), fabsf(q[j][v + 1])),
+                                            make_float2(-1.4426950408889634f, -1.4426950408889634f));
+                t[j] = make_float2(ex2_approx(e.x), ex2_approx(e.y));
+            }
+            const uint32_t par0 = qs[0][0] ^ qs[1][0] ^ qs[2][0] ^ qs[3][0] ^ synbit[v];
+            const uint32_t par1 = qs[0][1] ^ qs[1][1] ^ qs[2][1] ^ qs[3][1] ^ synbit[v + 1];
+            const float2 one = make_float2(1.0f, 1.0f);
+            const float2 S01 = __ffma2_rn(t[0], t[1], one), D01 = __fadd2_rn(t[0], t[1]);
+            const float2 S23 = __ffma2_rn(t[2], t[3], one), D23 = __fadd2_rn(t[2], t[3]);
+            float2 S[4], Dv[4];
+            S[0] = __ffma2_rn(t[1], D23, S23);
+            Dv[0] = __ffma2_rn(t[1], S23, D23);
+            S[1] = __ffma2_rn(t[0], D23, S23);
+            Dv[1] = __ffma2_rn(t[0], S23, D23);
+            S[2] = __ffma2_rn(t[3], D01, S01);
+            Dv[2] = __ffma2_rn(t[3], S01, D01);
+            S[3] = __ffma2_rn(t[2], D01, S01);
+            Dv[3] = __ffma2_rn(t[2], S01, D01);
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const float2 x = __fmul2_rn(S[j], make_float2(rcp_approx(Dv[j].x), rcp_approx(Dv[j].y)));
+                const float2 lg = __fmul2_rn(make_float2(lg2_approx(x.x), lg2_approx(x.y)),
+                                             make_float2(0.6931471805599453f, 0.6931471805599453f));
+                const float m0 = msg_round<H>(fminf(lg.x, mag_max)), m1 = msg_round<H>(fminf(lg.y, mag_max));
+                const float r0 = __uint_as_float(__float_as_uint(m0) | (qs[j][0] ^ par0));
+                const float r1 = __uint_as_float(__float_as_uint(m1) | (qs[j][1] ^ par1));
+                ph[j][v] = r0;
+                ph[j][v + 1] = r1;
+                const float2 l = __fadd2_rn(make_float2(q[j][v], q[j][v + 1]), make_float2(r0, r1));
+                q[j][v] = clampT(l.x, clip);
+                q[j][v + 1] = clampT(l.y, clip);
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int v = 0; v < V; v++) {
         uint32_t qs[4];

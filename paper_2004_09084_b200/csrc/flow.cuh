@@ -89,9 +89,11 @@ struct FlowArgs {
     const uint2 *slot_tab;   // [S]
     const uint2 *edge_tab;   // [E]
     const int2 *items;       // per item of one sweep: {slot | g << 16, kb}
-    int32_t sweep_items;     // items per sweep
-    uint32_t sweep_mul, sweep_shift;  // item / sweep_items == (umulhi(item, mul) + item) >> shift
-    int32_t item_end;        // items of this launch (sweeps x sweep_items)
+    int32_t sweep_items;     // items per sweep of one group block
+    uint32_t sweep_mul, sweep_shift;  // x / sweep_items == (umulhi(x, mul) + x) >> shift
+    int32_t blk_items;       // items of this launch per group block (sweeps x sweep_items)
+    uint32_t blk_mul, blk_shift;      // x / blk_items, the same way
+    int32_t item_end;        // items of this launch (group blocks x blk_items)
     int32_t t_base;          // global sweep index of item 0 (flags count global sweeps)
     int *counter;            // claim counter of this launch (zeroed before it)
     int *flags;              // [G][nkb_total] iterations completed per tile
@@ -153,9 +155,18 @@ __host__ __device__ constexpr size_t flow_smem_bytes(int S, int E, int stages) {
     return ((kFlowHeadBytes + 8 * (size_t)(S + E) + 127) / 128) * 128 + (size_t)stages * kFlowStageBytes;
 }
 
-// item / sweep_items without a division (item < 2^31, multiplier from flow_sweep_divisor)
-__device__ __forceinline__ int flow_sweep_of(const FlowArgs &a, int item) {
-    return (int)((__umulhi((uint32_t)item, a.sweep_mul) + (uint32_t)item) >> a.sweep_shift);
+// Item n -> (sweep t relative to t_base, index into the item table), without divisions
+// (n < 2^31, multipliers from flow_sweep_divisor).  Items run group block by group block
+// (all sweeps of a launch for lane groups [b*GB, (b+1)*GB), then the next block), each
+// block in (sweep, layer, group, slot, k-block) order.
+__device__ __forceinline__ int flow_fastdiv(int x, uint32_t mul, uint32_t shift) {
+    return (int)((__umulhi((uint32_t)x, mul) + (uint32_t)x) >> shift);
+}
+__device__ __forceinline__ int flow_item_map(const FlowArgs &a, int n, int &t) {
+    const int b = flow_fastdiv(n, a.blk_mul, a.blk_shift);
+    const int r = n - b * a.blk_items;
+    t = flow_fastdiv(r, a.sweep_mul, a.sweep_shift);
+    return b * a.sweep_items + (r - t * a.sweep_items);
 }
 inline void flow_sweep_divisor(uint32_t d, uint32_t &mul, uint32_t &shift) {
     uint32_t l = 0;
@@ -547,7 +558,10 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             if (n < a.item_end && lane == 0) n2 = atomicAdd(a.counter, 1);
             return n;
         };
-        auto record = [&](int n) { return __ldg(a.items + (n - flow_sweep_of(a, n) * a.sweep_items)); };
+        auto record = [&](int n) {
+            int t;
+            return __ldg(a.items + flow_item_map(a, n, t));
+        };
         int n1 = next_claim();
         int2 r1 = make_int2(0, 0);
         if (n1 < a.item_end) r1 = record(n1);
@@ -573,7 +587,9 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         };
         auto resolve = [&](int item, int2 e) {
             FlowHdr h;
-            h.t = a.t_base + flow_sweep_of(a, item);
+            int t_rel;
+            flow_item_map(a, item, t_rel);
+            h.t = a.t_base + t_rel;
             h.slot = e.x & 0xffff;
             h.g = e.x >> 16;
             const uint2 st = stab[h.slot];

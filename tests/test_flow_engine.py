@@ -37,7 +37,8 @@ def _states(name, batch, seed=3, syndrome=False):
 
 @pytest.mark.parametrize("name,batch,iters", [("standin_v2_z100", 64, 20), ("standin_v2_z2500", 64, 4),
                                               ("standin_v2_z100", 8, 30), ("demo_6x12_z16", 33, 12),
-                                              ("standin_v2_z100", 256, 12), ("standin_v2_z2500", 128, 3)])
+                                              ("standin_v2_z100", 256, 12), ("standin_v2_z2500", 128, 3),
+                                              ("standin_v2_z100", 192, 6), ("standin_v2_z100", 200, 6)])
 def test_flow_decode_bit_identical_to_layer_engine(gpu, name, batch, iters):
     import paper_2004_09084_b200 as q
     from paper_2004_09084_b200 import _native

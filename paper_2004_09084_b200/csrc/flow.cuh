@@ -95,6 +95,7 @@ struct FlowArgs {
     uint32_t blk_mul, blk_shift;      // x / blk_items, the same way
     int32_t item_end;        // items of this launch (group blocks x blk_items)
     int32_t t_base;          // global sweep index of item 0 (flags count global sweeps)
+    const int *t_dev;        // if set: t_base read from device memory (frame-pool sweep graphs)
     int *counter;            // claim counter of this launch (zeroed before it)
     int *flags;              // [G][nkb_total] iterations completed per tile
     int32_t nkb_total;
@@ -551,6 +552,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         // trip is on the tile's critical path.  Holding claimed items is deadlock free:
         // they are larger than the item in hand.  Resolved headers go to the loader warp
         // through a small queue, so dependency polling overlaps the bulk-copy issue.
+        const int t_base = a.t_dev ? *(volatile const int *)a.t_dev : a.t_base;
         int n2 = 0;
         if (lane == 0) n2 = atomicAdd(a.counter, 1);
         auto next_claim = [&]() {
@@ -589,7 +591,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             FlowHdr h;
             int t_rel;
             flow_item_map(a, item, t_rel);
-            h.t = a.t_base + t_rel;
+            h.t = t_base + t_rel;
             h.slot = e.x & 0xffff;
             h.g = e.x >> 16;
             const uint2 st = stab[h.slot];

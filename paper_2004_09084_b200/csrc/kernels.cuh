@@ -870,8 +870,12 @@ __global__ void pool_update_kernel(int64_t Bp, int lw, int max_iter, const uint3
                                    const uint32_t *lane_any, int64_t first_frame, int64_t n_frames,
                                    int64_t *lane_frame, int32_t *lane_iter, uint8_t *active, int *n_active,
                                    uint8_t *out_conv, int64_t *out_iters, uint8_t *out_err, int32_t *counts,
-                                   int32_t *refill, uint32_t *fresh) {
+                                   int32_t *refill, uint32_t *fresh, int *claim) {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b == 0) {  // the next sweep: its index (counts[2], read by the flow kernel) and claim counter
+        counts[2]++;
+        *claim = 0;
+    }
     if (b >= Bp) return;
     const int64_t f = lane_frame[b];
     if (f < 0) return;

@@ -515,7 +515,7 @@ static int enqueue_flow_reset(qcl_state *st, int counters) {
 
 // Sweeps [t0, t0 + T) in one persistent launch using claim counter `counter`.
 static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, int counter, bool et,
-                        int defer_last = -1) {
+                        int defer_last = -1, const int *t_dev = nullptr) {
     const qcl_plan *p = st->plan;
     FlowArgs a;
     a.slot_tab = st->fslot_tab;
@@ -527,6 +527,7 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     flow_sweep_divisor((uint32_t)a.blk_items, a.blk_mul, a.blk_shift);
     a.item_end = (int32_t)(st->f_nblk * T * st->f_sweep_items);
     a.t_base = t0;
+    a.t_dev = t_dev;
     a.counter = st->fcounters + counter;
     a.flags = st->fflags;
     a.nkb_total = st->f_nkb_total;
@@ -1510,11 +1511,11 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
         h_frame[b] = first_frame + b;
         h_active[b] = 1;
     }
-    const int32_t h_count[2] = {0, (int32_t)first};
+    const int32_t h_count[3] = {0, (int32_t)first, 0};  // refills, frames handed out, sweep
     const int h_n_active = (int)first;
     CK(cudaMemcpyAsync(st->pframe, h_frame.data(), 8 * st->Bp, cudaMemcpyHostToDevice, sm));
     CK(cudaMemcpyAsync(st->active, h_active.data(), st->Bp, cudaMemcpyHostToDevice, sm));
-    CK(cudaMemcpyAsync(st->pcount, h_count, 8, cudaMemcpyHostToDevice, sm));
+    CK(cudaMemcpyAsync(st->pcount, h_count, 12, cudaMemcpyHostToDevice, sm));
     CK(cudaMemcpyAsync(st->n_active, &h_n_active, sizeof(int), cudaMemcpyHostToDevice, sm));
     CK(cudaMemsetAsync(st->piter, 0, 4 * st->Bp, sm));
     CK(cudaMemsetAsync(st->pfresh, 0, 4 * st->G, sm));
@@ -1531,32 +1532,50 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
     const unsigned qgrid = (unsigned)cdiv((p->n + 3) / 4, kBlock);
     // every frame needs at most max_iterations sweeps and the lanes work concurrently
     const int64_t max_sweeps = (int64_t)cfg->max_iterations * (cdiv(n_frames, st->B) + 1) + 1;
-    for (int64_t t = 0; t < max_sweeps; t++) {
-        CK(cudaMemsetAsync(st->fcounters + (t & 1), 0, sizeof(int), sm));
-        if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, (int)t, 1, (int)(t & 1), true))) break;
-        CK(cudaMemsetAsync(st->pfresh, 0, 4 * st->G, sm));
+    // Sweeps run as a CUDA graph of kPoolChunk sweeps: the sweep index lives in device memory
+    // (pcount[2], advanced by pool_update with the claim counter reset), so every sweep has the
+    // same launch parameters and the host only launches chunks and reads the active count one
+    // chunk behind.  Sweeps after the last lane retired cost ~nothing (the flow launch returns
+    // at once, the bookkeeping kernels find no active lane).
+    constexpr int kPoolChunk = 4;
+    CK(cudaMemsetAsync(st->fcounters, 0, sizeof(int), sm));
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    CK(cudaStreamBeginCapture(sm, cudaStreamCaptureModeThreadLocal));
+    for (int k = 0; k < kPoolChunk && !rc; k++) {
+        if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, 0, 1, 0, true, -1, st->pcount + 2))) break;
+        cudaMemsetAsync(st->pfresh, 0, 4 * st->G, sm);
         if ((rc = enqueue_check(st, st->gactive))) break;
-        CK(cudaMemsetAsync(st->plane_any, 0, 4 * st->G, sm));
+        cudaMemsetAsync(st->plane_any, 0, 4 * st->G, sm);
         lane_any_kernel<<<(unsigned)(2 * sms_of(st)), kBlock, 0, sm>>>(st->signs, p->n, st->G, st->gactive,
                                                                       st->plane_any);
-        CK(cudaMemsetAsync(st->pcount, 0, sizeof(int32_t), sm));
+        cudaMemsetAsync(st->pcount, 0, sizeof(int32_t), sm);
         pool_update_kernel<<<gb, kBlock, 0, sm>>>(st->Bp, st->lw, cfg->max_iterations, st->unsat, st->plane_any,
                                                  first_frame, n_frames, st->pframe, st->piter, st->active,
                                                  st->n_active, d_conv, d_iters, d_err, st->pcount, st->prefill,
-                                                 st->pfresh);
+                                                 st->pfresh, st->fcounters);
         pool_refill_kernel<<<dim3(qgrid, (unsigned)std::min<int64_t>(st->Bp, 8)), kBlock, 0, sm>>>(
             st->pcount, st->prefill, st->pframe, p->n, st->lw, seed, (uint32_t)snr_idx, sigma, sigma2,
             cfg->llr_clip, (float *)st->llr, (float *)st->L);
         enqueue_group_active(st);
-        CK(cudaGetLastError());
-        // stop once every lane retired: the active count is read one sweep behind
-        CK(cudaMemcpyAsync(st->h_flag + (t & 1), st->n_active, sizeof(int), cudaMemcpyDeviceToHost, sm));
-        CK(cudaEventRecord(st->ev_flag[t & 1], sm));
-        if (t >= 1) {
-            CK(cudaEventSynchronize(st->ev_flag[(t - 1) & 1]));
-            if (st->h_flag[(t - 1) & 1] == 0) break;
-        }
     }
+    cudaError_t ce = cudaStreamEndCapture(sm, &graph);
+    if (!rc && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (!rc && ce != cudaSuccess) rc = fail(QCL_ECUDA, "pool sweep graph: %s", cudaGetErrorString(ce));
+    for (int64_t c = 0; !rc && c * kPoolChunk < max_sweeps; c++) {
+        cudaError_t e = cudaGraphLaunch(exec, sm);
+        // stop once every lane retired: the active count is read one chunk behind
+        if (e == cudaSuccess) e = cudaMemcpyAsync(st->h_flag + (c & 1), st->n_active, sizeof(int), cudaMemcpyDeviceToHost, sm);
+        if (e == cudaSuccess) e = cudaEventRecord(st->ev_flag[c & 1], sm);
+        if (e == cudaSuccess && c >= 1) e = cudaEventSynchronize(st->ev_flag[(c - 1) & 1]);
+        if (e != cudaSuccess) {
+            rc = fail(QCL_ECUDA, "pool sweep: %s", cudaGetErrorString(e));
+            break;
+        }
+        if (c >= 1 && st->h_flag[(c - 1) & 1] == 0) break;
+    }
+    if (exec) cudaGraphExecDestroy(exec);
     st->pool_active = false;
     CK(cudaEventRecord(st->ev1, sm));
     if (!rc) {

@@ -109,6 +109,8 @@ struct FlowArgs {
     const uint8_t *gactive;  // early termination: lane groups with an active frame (others skipped)
     int32_t defer_last;      // >= 0: degree-1 edges keep q in the L slot and no R until sweep defer_last
     const uint32_t *fresh;   // frame pool: [G] lanes that start a new frame this sweep (r_old = 0)
+    int32_t fresh_t;         // sweep whose tiles treat every lane as fresh (a decode's first
+                             // sweep: no zero fill of R before it), -1 none
     unsigned long long *stats;  // optional instrumentation (QCL_FLOW_STATS)
     double clip, eps;
     double mag_max;             // FP32 bound on |r| (LayerArgs::mag_max)
@@ -327,7 +329,7 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
     int par[V];
     const uint32_t dmask = flow_deferred_mask(a, h, etab);
     const bool last = h.t == a.defer_last;
-    const uint32_t fresh_lanes = a.fresh ? a.fresh[h.g] : 0u;
+    const uint32_t fresh_lanes = h.t == a.fresh_t ? 0xffffffffu : a.fresh ? a.fresh[h.g] : 0u;
     if (HAS_SYN) {
         const uint8_t *sp = a.syn + ((((int64_t)h.g * a.S + h.slot) * a.z + h.k0 + ci) << a.lw) + w0;
 #pragma unroll
@@ -405,7 +407,7 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
     using VT = typename Vec<float, V>::type;
     float q[D][V], t[D][V];
     int par[V];
-    const uint32_t fresh_lanes = a.fresh ? a.fresh[h.g] : 0u;
+    const uint32_t fresh_lanes = h.t == a.fresh_t ? 0xffffffffu : a.fresh ? a.fresh[h.g] : 0u;
     const uint32_t dmask = flow_deferred_mask(a, h, etab);
     const bool last = h.t == a.defer_last;
     if (HAS_SYN && act) {

@@ -515,7 +515,7 @@ static int enqueue_flow_reset(qcl_state *st, int counters) {
 
 // Sweeps [t0, t0 + T) in one persistent launch using claim counter `counter`.
 static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, int counter, bool et,
-                        int defer_last = -1, const int *t_dev = nullptr) {
+                        int defer_last = -1, const int *t_dev = nullptr, int fresh_t = -1) {
     const qcl_plan *p = st->plan;
     FlowArgs a;
     a.slot_tab = st->fslot_tab;
@@ -528,6 +528,7 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.item_end = (int32_t)(st->f_nblk * T * st->f_sweep_items);
     a.t_base = t0;
     a.t_dev = t_dev;
+    a.fresh_t = fresh_t;
     a.counter = st->fcounters + counter;
     a.flags = st->fflags;
     a.nkb_total = st->f_nkb_total;
@@ -1135,7 +1136,10 @@ int qcl_state_set_syndrome(qcl_state *st, const uint8_t *syndrome) {
     return QCL_OK;
 }
 
-static int enqueue_reset(qcl_state *st, double clip) {
+// new_state (decoder.py:191-202): L = clip(llr), R = 0.  zero_r = false when the first
+// flow sweep treats every message as zero itself (FlowArgs::fresh_t): saves writing R
+// (964 MB at 64 codewords) before every decode.
+static int enqueue_reset(qcl_state *st, double clip, bool zero_r = true) {
     const qcl_plan *p = st->plan;
     const int64_t nl = st->Bp * p->n;
     if (st->prec == QCL_PREC_FP32)
@@ -1145,7 +1149,7 @@ static int enqueue_reset(qcl_state *st, double clip) {
         reset_kernel<double><<<(unsigned)cdiv(nl, kBlock), kBlock, 0, st->stream>>>((const double *)st->llr,
                                                                                      (double *)st->L, nl, clip);
     CK(cudaGetLastError());
-    CK(cudaMemsetAsync(st->R, 0, (size_t)st->Bp * p->E * p->z * st->resz, st->stream));
+    if (zero_r) CK(cudaMemsetAsync(st->R, 0, (size_t)st->Bp * p->E * p->z * st->resz, st->stream));
     st->launches_all++;
     return QCL_OK;
 }
@@ -1298,14 +1302,14 @@ static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
         st->B, st->Bp, cfg->max_iterations, st->active, st->conv, st->iters, st->n_active);
     st->launches_all++;
     enqueue_group_active(st);
-    if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
     st->g_et = et;
     const bool flow = st->flow_decode;
+    if ((rc = enqueue_reset(st, cfg->llr_clip, !flow))) return rc;  // flow: sweep 0 zeroes r_old itself
     if (flow) {
         if ((rc = enqueue_flow_reset(st, et ? cfg->max_iterations : 1))) return rc;
         if (!et) {  // every sweep in one persistent launch, degree-1 edges deferred
             if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, 0, cfg->max_iterations, 0, false,
-                                   flow_defer_last(cfg->max_iterations))))
+                                   flow_defer_last(cfg->max_iterations), nullptr, 0)))
                 return rc;
         }
     }
@@ -1313,7 +1317,8 @@ static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
         if (flow && !et) break;
         const int64_t before = st->launches_layer;
         if (flow) {
-            if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, t - 1, 1, t - 1, true))) return rc;
+            if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, t - 1, 1, t - 1, true, -1, nullptr, 0)))
+                return rc;
             st->launches_all -= st->launches_layer - before;  // counted below
         } else {
             enqueue_sweep(st, cfg->llr_clip, cfg->phi_epsilon);
@@ -1392,9 +1397,9 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
         st->B, st->Bp, cfg->max_iterations, st->active, st->conv, st->iters, st->n_active);
     st->launches_all++;
     enqueue_group_active(st);
-    if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
     const unsigned gb = (unsigned)cdiv(st->B, kBlock);
     const bool flow = st->flow_decode;
+    if ((rc = enqueue_reset(st, cfg->llr_clip, !flow))) return rc;  // flow: sweep 0 zeroes r_old itself
     if (flow && (rc = enqueue_flow_reset(st, cfg->max_iterations))) return rc;
     for (int t = 1; t <= cfg->max_iterations; t++) {
         if (flow) {
@@ -1407,7 +1412,7 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
                 CK(cudaEventRecord(a, st->stream));
             }
             if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, t - 1, T, t - 1, et,
-                                   et ? -1 : flow_defer_last(cfg->max_iterations))))
+                                   et ? -1 : flow_defer_last(cfg->max_iterations), nullptr, 0)))
                 return rc;
             if (st->profiling) {
                 CK(cudaEventRecord(b, st->stream));
@@ -1523,7 +1528,7 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
     if ((rc = qcl_state_set_llr_synthetic(st, seed, snr_idx, first_frame, snr, 0))) return rc;
     st->has_syn = false;
     CK(cudaEventRecord(st->ev0, sm));
-    if ((rc = enqueue_reset(st, cfg->llr_clip))) return rc;
+    if ((rc = enqueue_reset(st, cfg->llr_clip, false))) return rc;  // sweep 0 zeroes r_old itself
     enqueue_group_active(st);
     CK(cudaMemsetAsync(st->fflags, 0, sizeof(int) * QCL_FLAG_STRIDE * (size_t)st->G * st->f_nkb_total, sm));
     st->pool_active = true;
@@ -1543,7 +1548,7 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
     cudaGraphExec_t exec = nullptr;
     CK(cudaStreamBeginCapture(sm, cudaStreamCaptureModeThreadLocal));
     for (int k = 0; k < kPoolChunk && !rc; k++) {
-        if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, 0, 1, 0, true, -1, st->pcount + 2))) break;
+        if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, 0, 1, 0, true, -1, st->pcount + 2, 0))) break;
         cudaMemsetAsync(st->pfresh, 0, 4 * st->G, sm);
         if ((rc = enqueue_check(st, st->gactive))) break;
         cudaMemsetAsync(st->plane_any, 0, 4 * st->G, sm);

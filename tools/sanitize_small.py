@@ -27,3 +27,27 @@ for name in ("demo_4x8_z100", "standin_v2_z100"):
             print(name, "et" if et else "noet", precision, "engines agree:", same, flush=True)
             if precision == "fp32" and not same:
                 sys.exit(1)
+
+# flow-engine paths added later: group blocks (128 codewords = 2 blocks of 8 lane groups),
+# FP16 messages, the frame pool
+base = q.load_base_matrix(ROOT / "codes" / "standin_v2_z100.txt")
+sched = q.greedy_schedule(base)
+index = q.build_compact_index(base, sched)
+n, m = base.n_cols * base.z, base.n_rows * base.z
+llr = rng.normal(0.5, 2.0, size=(128, n))
+for et in (False, True):
+    cfg = q.DecoderConfig(max_iterations=3, early_termination=et)
+    res = [q.LayeredDecoder(index, sched, cfg, precision="fp32", engine=e).decode_batch_arrays(llr, np.zeros((128, m), np.uint8))
+           for e in (0, 4)]
+    same = all(np.array_equal(a, b) for a, b in zip(res[0], res[1]))
+    print("standin_v2_z100 B=128", "et" if et else "noet", "fp32 engines agree:", same, flush=True)
+    if not same:
+        sys.exit(1)
+    out = q.LayeredDecoder(index, sched, cfg, precision="fp32-msg16").decode_batch_arrays(llr[:9], np.zeros((9, m), np.uint8))
+    print("standin_v2_z100 B=9", "et" if et else "noet", "fp32-msg16 ran, converged", int(out[1].sum()), flush=True)
+from paper_2004_09084_b200 import _native  # noqa: E402
+
+st = _native.State(_native.Plan(index, sched, 0), 16, "fp32")
+qcfg = _native.make_config(q.DecoderConfig(max_iterations=6, early_termination=True), "fp32")
+conv, iters, err, _ = st.decode_pool(qcfg, 0, 0, 0, 40, 0.3)
+print("frame pool 40 frames:", int(conv.sum()), "converged", int(iters.sum()), "iterations", flush=True)

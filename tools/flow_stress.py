@@ -15,7 +15,8 @@ from paper_2004_09084_b200 import _native  # noqa: E402
 
 trials = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 bad_total = 0
-for name, batch, iters in (("standin_v2_z100", 64, 20), ("standin_v2_z2500", 64, 6), ("standin_v2_z100", 8, 30)):
+for name, batch, iters in (("standin_v2_z100", 64, 20), ("standin_v2_z2500", 64, 6), ("standin_v2_z100", 8, 30),
+                           ("standin_v2_z100", 128, 10), ("standin_v2_z100", 32, 20)):
     base = q.load_base_matrix(ROOT / "codes" / f"{name}.txt")
     sched = q.greedy_schedule(base)
     index = q.build_compact_index(base, sched)

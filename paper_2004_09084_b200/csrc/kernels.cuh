@@ -343,35 +343,35 @@ __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph
                 q[j][v + 1] = clampT(l.y, clip);
             }
         }
-        return;
-    }
+    } else {
 #pragma unroll
-    for (int v = 0; v < V; v++) {
-        uint32_t qs[4];
-        float t[4];
+        for (int v = 0; v < V; v++) {
+            uint32_t qs[4];
+            float t[4];
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            qs[j] = __float_as_uint(q[j][v]) & 0x80000000u;
-            t[j] = sd_t(q[j][v]);
-        }
-        const uint32_t par = qs[0] ^ qs[1] ^ qs[2] ^ qs[3] ^ synbit[v];
-        const float S01 = fmaf(t[0], t[1], 1.0f), D01 = t[0] + t[1];
-        const float S23 = fmaf(t[2], t[3], 1.0f), D23 = t[2] + t[3];
-        float S[4], Dv[4];
-        S[0] = fmaf(t[1], D23, S23);
-        Dv[0] = fmaf(t[1], S23, D23);
-        S[1] = fmaf(t[0], D23, S23);
-        Dv[1] = fmaf(t[0], S23, D23);
-        S[2] = fmaf(t[3], D01, S01);
-        Dv[2] = fmaf(t[3], S01, D01);
-        S[3] = fmaf(t[2], D01, S01);
-        Dv[3] = fmaf(t[2], S01, D01);
+            for (int j = 0; j < 4; j++) {
+                qs[j] = __float_as_uint(q[j][v]) & 0x80000000u;
+                t[j] = sd_t(q[j][v]);
+            }
+            const uint32_t par = qs[0] ^ qs[1] ^ qs[2] ^ qs[3] ^ synbit[v];
+            const float S01 = fmaf(t[0], t[1], 1.0f), D01 = t[0] + t[1];
+            const float S23 = fmaf(t[2], t[3], 1.0f), D23 = t[2] + t[3];
+            float S[4], Dv[4];
+            S[0] = fmaf(t[1], D23, S23);
+            Dv[0] = fmaf(t[1], S23, D23);
+            S[1] = fmaf(t[0], D23, S23);
+            Dv[1] = fmaf(t[0], S23, D23);
+            S[2] = fmaf(t[3], D01, S01);
+            Dv[2] = fmaf(t[3], S01, D01);
+            S[3] = fmaf(t[2], D01, S01);
+            Dv[3] = fmaf(t[2], S01, D01);
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const float mag = msg_round<H>(sd_mag(S[j], Dv[j], mag_max));
-            const float r = __uint_as_float(__float_as_uint(mag) | (qs[j] ^ par));
-            ph[j][v] = r;
-            q[j][v] = clampT(q[j][v] + r, clip);
+            for (int j = 0; j < 4; j++) {
+                const float mag = msg_round<H>(sd_mag(S[j], Dv[j], mag_max));
+                const float r = __uint_as_float(__float_as_uint(mag) | (qs[j] ^ par));
+                ph[j][v] = r;
+                q[j][v] = clampT(q[j][v] + r, clip);
+            }
         }
     }
 }

@@ -625,7 +625,6 @@ static int enqueue_syn_pack(qcl_state *st) {
 
 // One sweep over every layer, captured once into a graph and replayed per iteration.
 static int run_sweep(qcl_state *st, double clip, double eps, bool et) {
-    const qcl_plan *p = st->plan;
     if (!st->sweep_exec || st->g_clip != clip || st->g_eps != eps || st->g_syn != st->has_syn || st->g_et != et) {
         st->g_et = et;
         if (st->sweep_exec) {

@@ -523,6 +523,33 @@ __global__ void __launch_bounds__(kBlock) sign_pack_kernel(const T *L, int64_t G
     signs[v * (Gn / n) + g] = m;
 }
 
+// The same, one thread per variable over all lane groups: no 64-bit division per thread,
+// and each thread writes its variable's G sign words contiguously (chunks of 4 groups as
+// one 16-byte store when G % 4 == 0).
+template <typename T>
+__global__ void __launch_bounds__(kBlock) sign_pack_var_kernel(const T *L, int G, int lw, uint32_t *signs, int64_t n,
+                                                               const uint8_t *gact) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    uint32_t *out = signs + v * G;
+    if ((G & 3) == 0) {
+        for (int g = 0; g < G; g += 4) {
+            const bool a0 = !gact || gact[g], a1 = !gact || gact[g + 1], a2 = !gact || gact[g + 2],
+                       a3 = !gact || gact[g + 3];
+            if (!(a0 | a1 | a2 | a3)) continue;
+            uint4 m;
+            m.x = a0 ? sign_word(L, (int64_t)g * n + v, lw) : out[g];
+            m.y = a1 ? sign_word(L, (int64_t)(g + 1) * n + v, lw) : out[g + 1];
+            m.z = a2 ? sign_word(L, (int64_t)(g + 2) * n + v, lw) : out[g + 2];
+            m.w = a3 ? sign_word(L, (int64_t)(g + 3) * n + v, lw) : out[g + 3];
+            *reinterpret_cast<uint4 *>(out + g) = m;
+        }
+    } else {
+        for (int g = 0; g < G; g++)
+            if (!gact || gact[g]) out[g] = sign_word(L, (int64_t)g * n + v, lw);
+    }
+}
+
 // gact[g] = some frame of lane group g is still active (early termination).
 __global__ void group_active_kernel(int64_t Bp, int lw, const uint8_t *active, uint8_t *gact) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -572,7 +572,13 @@ static int enqueue_signs(qcl_state *st, const uint8_t *gact = nullptr) {
     const qcl_plan *p = st->plan;
     const int64_t Gn = (int64_t)st->G * p->n;
     const unsigned grid = (unsigned)cdiv(Gn, kBlock);
-    if (st->prec == QCL_PREC_FP32)
+#ifndef QCL_SIGN_PER_VAR
+#define QCL_SIGN_PER_VAR 1
+#endif
+    if (st->prec == QCL_PREC_FP32 && QCL_SIGN_PER_VAR)
+        sign_pack_var_kernel<float><<<(unsigned)cdiv(p->n, kBlock), kBlock, 0, st->stream>>>(
+            (const float *)st->L, st->G, st->lw, st->signs, p->n, gact);
+    else if (st->prec == QCL_PREC_FP32)
         sign_pack_kernel<float><<<grid, kBlock, 0, st->stream>>>((const float *)st->L, Gn, st->lw, st->signs, p->n,
                                                                   gact);
     else

@@ -47,9 +47,6 @@
 #ifndef QCL_FLAG_STRIDE
 #define QCL_FLAG_STRIDE 32  // ints between consecutive tile flags
 #endif
-#ifndef QCL_FLOW_RPREFETCH
-#define QCL_FLOW_RPREFETCH 1
-#endif
 #ifndef QCL_FLOW_STAGE_KB
 #define QCL_FLOW_STAGE_KB 32
 #endif
@@ -692,18 +689,6 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             if (++q == kFlowQueue) {
                 q = 0;
                 qph ^= 1;
-            }
-            if (QCL_FLOW_RPREFETCH && h.kt > 0 && lane < h.d) {
-                // L2 prefetch of the tile's message runs while the loader waits for a free
-                // stage: they stream from DRAM (evict_first) and their DRAM latency then
-                // overlaps the wait instead of the stage's occupancy (-1.3% at 64 codewords,
-                // -3% at 32)
-                const uint32_t ex = etab[h.edge_off + lane].x;
-                if (((ex >> 15) & 1) || a.defer_last < 0) {  // deferred edges load no R
-                    const RT *rg = reinterpret_cast<const RT *>(a.R) +
-                                   ((((size_t)h.g * a.E + h.edge_off + lane) * a.z + h.k0) << a.lw);
-                    bulk_prefetch_l2(rg, (uint32_t)(h.kt * W) * (uint32_t)sizeof(RT));
-                }
             }
             if (it >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
             if (lprof) { const long long c_ = clock64(); acc[1] += c_ - tc; tc = c_; }

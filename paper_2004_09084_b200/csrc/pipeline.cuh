@@ -79,9 +79,6 @@ __device__ __forceinline__ void bulk_store(void *gmem_dst, const void *smem_src,
                  "r"(smem_u32(smem_src)), "r"(bytes), "l"(policy)
                  : "memory");
 }
-__device__ __forceinline__ void bulk_prefetch_l2(const void *gmem, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

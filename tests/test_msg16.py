@@ -88,13 +88,13 @@ def test_sweeps_within_fp16_rounding_of_fp32(gpu, name, batch, sweeps, syn):
     # layers see the posteriors those errors moved.  Measured on B200 (tools/msg16_diag.py):
     # max |dL| = max |dR| = 0.008-0.009 after one sweep, 0.023 after three (zero target),
     # 0.032 after two with a random target syndrome; mean |dL| 1e-4..6e-4 (2e-3 with the
-    # random target); sign flips
-    # 0..2.6e-5 of the posteriors (near-zero values at SNR 0.5; 1 of 6336 on the 192-bit code).
+    # random target); sign flips 0..2.6e-5 of the posteriors (near-zero values at SNR 0.5),
+    # 2.8e-4 with a random target (many posteriors near zero; 1 of 6336 on the 192-bit code).
     tol = 0.02 * sweeps ** 2
     assert np.max(np.abs(lb - la)) <= tol and np.max(np.abs(rb - ra)) <= tol
     assert np.mean(np.abs(lb - la)) <= 2e-3 * sweeps and np.mean(np.abs(rb - ra)) <= 2e-3 * sweeps
     flips = np.count_nonzero((la < 0) != (lb < 0))
-    assert flips <= max(2, 1e-4 * la.size), flips
+    assert flips <= max(2, (5e-4 if syn else 1e-4) * la.size), flips
 
 
 @pytest.mark.gpu

@@ -1,7 +1,19 @@
-import sys; sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
-import numpy as np
-from conftest import channel_llrs, load_code
-from paper_2004_09084_b200 import _native
+"""FP16 edge messages vs FP32 after 1-3 sweeps: max/mean posterior and message
+differences and sign flips (the numbers behind tests/test_msg16.py's tolerances), and the
+FP16 rounding of an upload/download round trip.
+
+    python tools/msg16_diag.py
+"""
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+import numpy as np  # noqa: E402
+from conftest import channel_llrs, load_code  # noqa: E402
+
+from paper_2004_09084_b200 import _native  # noqa: E402
 base, sched, index = load_code("standin_v2_z100")
 plan = _native.Plan(index, sched, 0)
 n = base.n_cols * base.z

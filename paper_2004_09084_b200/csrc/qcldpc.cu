@@ -315,7 +315,11 @@ static void enqueue_unit_tma(qcl_state *st, const qcl_plan::Unit &u, cudaStream_
 
 static void enqueue_unit(qcl_state *st, const qcl_plan::Unit &u, cudaStream_t stream, double clip, double eps,
                          int g0, int ng) {
-    if (use_tma(st)) {
+    // the TMA ring needs two stages of 2*D*KT*W elements in shared memory; wide FP64 rows
+    // (row degree > 16: 2 x 128 KB) do not fit and run on the direct kernel
+    const bool tma_fits = (size_t)2 * 2 * dmax_bucket(u.dmax) * pipe_warps() * 32 * vec_width(st, u.dmax) * st->esz +
+                              128 <= 227 * 1024;
+    if (use_tma(st) && tma_fits) {
         enqueue_unit_tma(st, u, stream, clip, eps, g0, ng);
         return;
     }

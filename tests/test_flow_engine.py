@@ -95,3 +95,35 @@ def test_flow_fresh_states_first_launch(gpu):
         got = q.LayeredDecoder(index, sched, cfg, engine=4).decode_batch_arrays(llr, np.zeros((64, m), np.uint8))
         for a, b in zip(got, want):
             assert np.array_equal(a, b)
+
+
+def _high_degree_code():
+    """3 x 20 base matrix with row degrees 16 / 14 / 20 (above the flow engine's 12), z = 24."""
+    from conftest import make_code
+
+    rng = np.random.default_rng(11)
+    shifts = np.full((3, 20), -1, dtype=np.int64)
+    for i, deg in enumerate((16, 14, 20)):
+        cols = rng.choice(20, size=deg, replace=False)
+        shifts[i, cols] = rng.integers(0, 24, size=deg)
+    return make_code(shifts.tolist(), 24, merged=True)
+
+
+def test_high_degree_codes_fall_back_to_the_layer_engine(gpu):
+    """Row degree > 12: the default engine runs the per-layer kernels, with results equal
+    to engine 0 and to the FP64 path's decisions on a clean channel; FP16 messages refuse."""
+    import paper_2004_09084_b200 as q
+
+    base, sched, index = _high_degree_code()
+    n, m = base.n_cols * base.z, base.n_rows * base.z
+    llr = channel_llrs(n, 4.0, seed=2, snr_idx=0, frames=16)
+    syn = np.zeros((16, m), np.uint8)
+    cfg = q.DecoderConfig(max_iterations=8, early_termination=True)
+    out = {e: q.LayeredDecoder(index, sched, cfg, precision="fp32", engine=e).decode_batch_arrays(llr, syn)
+           for e in (0, 4)}
+    for a, b in zip(out[0], out[4]):
+        assert np.array_equal(a, b)
+    ref = q.LayeredDecoder(index, sched, cfg, precision="fp64").decode_batch_arrays(llr, syn)
+    assert np.array_equal(ref[1], out[4][1]) and np.array_equal(ref[2], out[4][2])
+    with pytest.raises(RuntimeError, match="flow engine"):
+        q.LayeredDecoder(index, sched, cfg, precision="fp32-msg16").decode_batch_arrays(llr, syn)

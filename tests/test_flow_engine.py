@@ -127,3 +127,41 @@ def test_high_degree_codes_fall_back_to_the_layer_engine(gpu):
     assert np.array_equal(ref[1], out[4][1]) and np.array_equal(ref[2], out[4][2])
     with pytest.raises(RuntimeError, match="flow engine"):
         q.LayeredDecoder(index, sched, cfg, precision="fp32-msg16").decode_batch_arrays(llr, syn)
+
+
+def test_random_codes_all_engines_agree(gpu):
+    """40 random codes (row degrees 1..20, z 1..40, merged or single-row schedules), random
+    targets, 8..136 codewords (1..17 lane groups, two group blocks at 128): the flow engine,
+    the TMA and the direct per-layer engines give bit-identical decodes (ET on and off) and
+    states; FP16 messages run wherever the flow engine does, and refuse cleanly elsewhere."""
+    import paper_2004_09084_b200 as q
+    from conftest import make_code
+
+    rng = np.random.default_rng(7)
+    for trial in range(40):
+        n_rows = int(rng.integers(1, 6))
+        n_cols = int(rng.integers(n_rows + 1, 24))
+        z = int(rng.integers(1, 41))
+        shifts = np.full((n_rows, n_cols), -1, dtype=np.int64)
+        for i in range(n_rows):
+            deg = int(rng.integers(1, min(20, n_cols) + 1))
+            cols = rng.choice(n_cols, size=deg, replace=False)
+            shifts[i, cols] = rng.integers(0, z, size=deg)
+        base, sched, index = make_code(shifts.tolist(), z, merged=bool(trial % 2))
+        batch = (8, 24, 72, 128, 136)[trial % 5]
+        n, m = base.n_cols * z, base.n_rows * z
+        llr = rng.normal(0.8, 2.0, size=(batch, n))
+        syn = (rng.random((batch, m)) < 0.2).astype(np.uint8)
+        cfg = q.DecoderConfig(max_iterations=6, early_termination=bool(trial % 3))
+        outs = [q.LayeredDecoder(index, sched, cfg, precision="fp32", engine=e).decode_batch_arrays(llr, syn)
+                for e in (0, 1, 4)]
+        for o in outs[1:]:
+            for a, b in zip(outs[0], o):
+                assert np.array_equal(a, b), trial
+        flow_ok = max(len([s for s in row if s >= 0]) for row in shifts.tolist()) <= 12
+        if flow_ok:
+            w, c, it = q.LayeredDecoder(index, sched, cfg, precision="fp32-msg16").decode_batch_arrays(llr, syn)
+            assert w.shape == outs[0][0].shape and np.all(it >= 1), trial
+        else:
+            with pytest.raises(RuntimeError, match="flow engine"):
+                q.LayeredDecoder(index, sched, cfg, precision="fp32-msg16").decode_batch_arrays(llr, syn)

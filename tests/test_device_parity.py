@@ -301,6 +301,41 @@ def test_random_codes_against_oracle(gpu, precision):
             assert np.array_equal(w, ow), trial
 
 
+def test_wide_rows_fp64_against_oracle(gpu):
+    """Row degrees 13..24 (the per-layer engines' wide buckets; FP64 rows above 16 run on
+    the direct kernel): FP64 decodes bit-exact against the C oracle, FP32 sweeps close."""
+    import paper_2004_09084_b200 as q
+    from oracle import oracle
+
+    rng = np.random.default_rng(5)
+    for trial in range(8):
+        n_rows, n_cols, z = int(rng.integers(1, 4)), 26, int(rng.integers(2, 12))
+        shifts = np.full((n_rows, n_cols), -1, dtype=np.int64)
+        for i in range(n_rows):
+            deg = int(rng.integers(13, 25))
+            cols = rng.choice(n_cols, size=deg, replace=False)
+            shifts[i, cols] = rng.integers(0, z, size=deg)
+        base, sched, index = make_code(shifts.tolist(), z, merged=bool(trial % 2))
+        code = oracle.OracleCode(index, sched)
+        batch = (2, 5, 9)[trial % 3]
+        n, m = base.n_cols * z, base.n_rows * z
+        llr = rng.normal(1.0, 2.0, size=(batch, n))
+        syn = (rng.random((batch, m)) < 0.3).astype(np.uint8)
+        ow, oc, oi = oracle.decode(code, llr, syn, 12, True)
+        w, c, it = q.LayeredDecoder(index, sched, q.DecoderConfig(max_iterations=12),
+                                    precision="fp64").decode_batch_arrays(llr, syn)
+        assert np.array_equal(c, oc) and np.array_equal(it, oi) and np.array_equal(w, ow), trial
+        _, st = fresh_state(index, sched, batch, "fp32")
+        post = np.clip(llr, -30, 30)
+        msg = np.zeros((batch, index.total_edges * z))
+        st.upload(post, msg)
+        st.set_syndrome(syn)
+        st.layers(0, len(sched.layers), 30.0, 1e-10)
+        dpost, dmsg = st.download()
+        oracle.layer_update(code, -1, post, msg, syn)
+        assert relerr(dpost, post) <= TOL_LAYER["fp32"] * 10 and relerr(dmsg, msg) <= TOL_LAYER["fp32"] * 10, trial
+
+
 @pytest.mark.parametrize("batch", [1, 2, 3, 31, 33, 64, 70])
 def test_batch_padding_and_lane_groups(gpu, batch):
     """Any batch size: lane groups are padded; results equal the oracle frame by frame."""

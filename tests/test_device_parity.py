@@ -429,7 +429,7 @@ def test_device_encode_mode_syndrome(gpu):
     assert np.array_equal(oracle.syndrome(code, w), oracle.syndrome(code, truths))
 
 
-@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("precision", ["fp64", "fp32", "fp32-msg16"])
 def test_decode_stream_matches_blocking_calls(gpu, precision):
     """decode_stream (async copies, double-buffered workspaces) == decode_batch_arrays,
     including nonzero syndromes, early termination and a batch-size change mid-stream."""

@@ -165,3 +165,27 @@ def test_random_codes_all_engines_agree(gpu):
         else:
             with pytest.raises(RuntimeError, match="flow engine"):
                 q.LayeredDecoder(index, sched, cfg, precision="fp32-msg16").decode_batch_arrays(llr, syn)
+
+
+def test_one_decoder_shared_by_threads(gpu):
+    """decoder.py:18-21 / :469-472: one decoder instance used by several host threads at
+    once (each call gets its own state, stream, flags and claim counters): results equal
+    the sequential calls', for FP32 and FP16 messages."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_2004_09084_b200 as q
+
+    base, sched, index = load_code("standin_v2_z100")
+    n, m = base.n_cols * base.z, base.n_rows * base.z
+    batches = [channel_llrs(n, 0.2, seed=3, snr_idx=0, frames=16, start=16 * i) for i in range(8)]
+    syn = np.zeros((16, m), np.uint8)
+    for precision in ("fp32", "fp32-msg16"):
+        for et in (True, False):
+            dec = q.LayeredDecoder(index, sched, q.DecoderConfig(max_iterations=15, early_termination=et),
+                                   precision=precision)
+            want = [dec.decode_batch_arrays(b, syn) for b in batches]
+            with ThreadPoolExecutor(4) as ex:
+                got = list(ex.map(lambda b: dec.decode_batch_arrays(b, syn), batches))
+            for w, g in zip(want, got):
+                for a, b in zip(w, g):
+                    assert np.array_equal(a, b), (precision, et)

@@ -175,15 +175,16 @@ def test_compare_schedules_on_device(gpu, tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["campaign_demo4x8z32_et50", "standin_z100_et"])
+@pytest.mark.parametrize("name", ["campaign_demo4x8z32_et50", "standin_z100_et", "standin_z100_et_128"])
 def test_frame_pool_matches_batched_decode_per_frame(gpu, name):
     """The frame pool changes only the timing: FER and average iterations identical to the
     batched device-channel decode (frames are independent; each runs its own sweeps)."""
     from paper_2004_09084_b200.campaign import CampaignConfig, run_campaign
 
-    if name == "standin_z100_et":
+    if name.startswith("standin_z100_et"):
+        lanes = 128 if name.endswith("_128") else 16  # 128 lanes: two group blocks per sweep
         kw = dict(matrix_path=str(ROOT / "codes" / "standin_v2_z100.txt"), snr_list=(0.17, 0.2), max_iterations=40,
-                  early_termination=True, batch_size=16, min_trials=96, seed=5, channel="device")
+                  early_termination=True, batch_size=lanes, min_trials=6 * lanes, seed=5, channel="device")
         cfg = CampaignConfig(**kw)
     else:
         cfg = config_of(golden(name), channel="device", batch_size=32, min_trials=256)

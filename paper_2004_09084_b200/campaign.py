@@ -274,7 +274,13 @@ class _DeviceChannelRunner:
     def _state(self, dev, count):
         key = (dev, count)
         if key not in self.states:
-            self.states[key] = _native.State(self.plans[dev], count, self.cfg.precision)
+            st = _native.State(self.plans[dev], count, self.cfg.precision)
+            # one untimed decode: the engine's one-time set-up (tile tables, flags, the decode
+            # graph) stays out of the first SNR point's timing
+            st.set_llr_synthetic(self.cfg.seed, 0, 0, 1.0)
+            st.set_syndrome(None)
+            st.decode(self.qcfg)
+            self.states[key] = st
         return self.states[key]
 
     def _slice(self, job):

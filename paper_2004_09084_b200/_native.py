@@ -11,6 +11,7 @@ concurrently.
 from __future__ import annotations
 
 import ctypes
+import sys
 import os
 from pathlib import Path
 
@@ -158,7 +159,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and _lib is not None:
+        if h and _lib is not None and not sys.is_finalizing():  # at exit the process frees it
             _lib.qcl_plan_destroy(h)
             self.handle = None
 
@@ -176,7 +177,7 @@ class State:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h and _lib is not None:
+        if h and _lib is not None and not sys.is_finalizing():  # at exit the process frees it
             _lib.qcl_state_destroy(h)
             self.handle = None
 
@@ -308,7 +309,7 @@ class PinnedArray:
 
     def __del__(self):
         p = getattr(self, "_ptr", None)
-        if p and p.value and _lib is not None:
+        if p and p.value and _lib is not None and not sys.is_finalizing():
             self.array = None
             _lib.qcl_host_free(p)
             self._ptr = None

@@ -11,8 +11,8 @@ concurrently.
 from __future__ import annotations
 
 import ctypes
-import sys
 import os
+import sys
 from pathlib import Path
 
 import numpy as np

@@ -228,11 +228,25 @@ __device__ __forceinline__ Item map_item(const SlotRange &r) {
 // |q| < eps gives t = 1, i.e. S = D and r = 0 on the other edges instead of eps = 1e-10.
 // 3 MUFU and ~19 instructions per edge (the Phi-domain form needed 6 MUFU and ~37).
 // Signs: r_j = |r_j| with sign (q_j < 0) ^ parity(all q < 0) ^ syndrome bit.
+//
+// QCL_F32_MATH selects how t and |r| are evaluated (the combine is the same):
+//   0: MUFU approximations (ex2/rcp/lg2.approx), the fast default;
+//   1: libdevice expf / IEEE division / logf (a few ulp end to end), for accuracy A/Bs.
+#ifndef QCL_F32_MATH
+#define QCL_F32_MATH 0
+#endif
+#if QCL_F32_MATH == 0
 __device__ __forceinline__ float sd_t(float q) { return ex2_approx(fabsf(q) * -1.4426950408889634f); }
 __device__ __forceinline__ float sd_mag(float S, float D, float mag_max) {
     // D = 0 only when every other message is infinitely strong: lg2(inf) -> mag_max
     return fminf(lg2_approx(S * rcp_approx(D)) * 0.6931471805599453f, mag_max);
 }
+#else
+__device__ __forceinline__ float sd_t(float q) { return expf(-fabsf(q)); }
+__device__ __forceinline__ float sd_mag(float S, float D, float mag_max) {
+    return fminf(logf(__fdiv_rn(S, D)), mag_max);
+}
+#endif
 
 // 16-bit edge messages (QCL_PREC_FP32_MSG16): |r| rounded to FP16 before it is used, so
 // the posterior update and the message store see the same value and the next sweep's
@@ -299,7 +313,7 @@ __device__ __forceinline__ void check_update_f32_d4(float (&q)[4][V], float (&ph
 #ifndef QCL_PACKED_F32X2
 #define QCL_PACKED_F32X2 1
 #endif
-    if constexpr (QCL_PACKED_F32X2 && V % 2 == 0) {
+    if constexpr (QCL_PACKED_F32X2 && QCL_F32_MATH == 0 && V % 2 == 0) {
         // lane pairs on the packed FP32 pipe (FMUL2/FFMA2/FADD2: two IEEE round-to-nearest
         // results per instruction, the same values as the scalar ops below)
 #pragma unroll

@@ -8,9 +8,10 @@ stated next to each assertion:
     log1p/expm1; hard decisions, convergence flags and
     iteration counts bit-exact.
   * FP32 path: one layer / one sweep within 2e-5, five sweeps within 1e-4
-    (north-star tolerance); hard decisions after short decodes bit-exact; long no-ET
-    decodes in the chaotic pre-convergence regime are compared by mismatch counts
-    (DESIGN.md section 4 explains why no FP32 implementation can be bit-exact there).
+    (north-star tolerance); hard decisions bit-exact after short decodes and after
+    50 no-ET iterations in the pre-convergence regime (SNR 0.161); only no-ET decodes
+    that run on past convergence into the clip-saturation regime (SNR 0.2) are
+    compared by frame-level outcome.
 """
 
 import hashlib
@@ -191,24 +192,44 @@ def test_decode_fp64_bit_exact(gpu, tag):
 
 @pytest.mark.parametrize("tag", DECODE_CASES)
 def test_decode_fp32_against_reference(gpu, tag):
-    """FP32 contract:
+    """FP32 contract, by regime:
       * early-termination runs and 10-iteration runs: converged flags and iteration
-        counts bit-exact, hard decisions bit-exact for every converged frame (and for
-        every frame of the 10-iteration runs);
-      * 50 no-ET iterations at SNR 0.161/0.2 (non-converging / post-convergence
-        saturation regime): FP32 and FP64 trajectories separate
-        chaotically, so only the frame-level outcome is compared -- convergence flags
-        must agree on >= 75% of frames; bit mismatches are reported."""
+        counts identical, hard decisions bit-exact (every converged frame, every frame
+        of the 10-iteration runs);
+      * 50 no-ET iterations at SNR 0.161 (pre-convergence): flags and iterations
+        identical, hard decisions identical wherever the reference posterior satisfies
+        |L| >= 1e-3 (the FP32 margin of tests/test_bench_config_parity.py);
+      * 50 no-ET iterations at SNR 0.2 (frames converge and then keep iterating into
+        the LLR-clip saturation regime): FP32 and FP64 trajectories
+        separate chaotically after convergence, so only the frame-level outcome is
+        compared -- convergence flags agree on >= 75% of frames; bit mismatches are
+        reported."""
     g, w, c, it, ref_w = run_golden_decode(tag, "fp32")
     ref_c = g["converged"]
     flips = int((w != ref_w).sum())
     frames_differ = int((w != ref_w).any(axis=1).sum())
     print(f"{tag}: fp32 bit mismatches {flips} in {frames_differ} frames; "
           f"converged {int(c.sum())} vs reference {int(ref_c.sum())}")
-    if bool(g["et"]) or "it10" in tag:
+    if bool(g["et"]):
         assert np.array_equal(c, ref_c) and np.array_equal(it, g["iterations"])
-        decided = ref_c if bool(g["et"]) else np.ones_like(ref_c)
-        assert np.array_equal(w[decided], ref_w[decided])
+        assert np.array_equal(w[ref_c], ref_w[ref_c])
+    elif "it10" in tag:
+        assert np.array_equal(c, ref_c) and np.array_equal(it, g["iterations"])
+        assert flips == 0
+    elif "snr0.161" in tag:
+        # 50 iterations amplify the FP32 state's rounding (tests/test_bench_config_parity.py):
+        # decisions identical wherever the reference posterior is not within 1e-3 of zero
+        assert np.array_equal(c, ref_c) and np.array_equal(it, g["iterations"])
+        from oracle import oracle
+
+        base, sched, index = load_code("standin_v2_z100")
+        llr = channel_llrs(base.n_cols * base.z, float(g["snr"]), int(g["seed"]), int(g["snr_idx"]), len(c))
+        ow, _, _, opost = oracle.decode(oracle.OracleCode(index, sched), llr, None, int(g["iters"]), False,
+                                        want_posterior=True)
+        assert np.array_equal(ow, ref_w)  # the oracle reproduces the reference's decisions
+        margin = np.abs(opost[w != ref_w])
+        print(f"{tag}: reference |L| at the flips {np.sort(margin).tolist()}")
+        assert (margin < 1e-3).all()
     else:
         assert (c == ref_c).mean() >= 0.75
 
@@ -217,7 +238,7 @@ def test_decode_fp32_against_reference(gpu, tag):
 def test_posterior_after_decode(gpu, precision):
     """Posterior after 10 and 50 sweeps (SNR 0.161, z=100 twin) vs the reference."""
     for tag, tol in [("decode_standin_z100_snr0.161_it10_noet", {"fp64": 1e-9, "fp32": 1e-4}),
-                     ("decode_standin_z100_snr0.161_it50_noet", {"fp64": 1e-6, "fp32": None})]:
+                     ("decode_standin_z100_snr0.161_it50_noet", {"fp64": 1e-6, "fp32": 1e-3})]:
         g = np.load(GOLDEN / f"{tag}.npz")
         base, sched, index = load_code("standin_v2_z100")
         n = base.n_cols * base.z
@@ -231,8 +252,7 @@ def test_posterior_after_decode(gpu, precision):
         post, _ = st.download()
         err = relerr(post, g["posterior"])
         print(f"{tag} {precision}: max rel posterior error {err:.3g}")
-        if tol[precision] is not None:
-            assert err <= tol[precision]
+        assert err <= tol[precision]
 
 
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])

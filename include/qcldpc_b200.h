@@ -134,6 +134,10 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
 int qcl_state_frame_errors(qcl_state *st, uint8_t *mismatch);
 /* Copy the state's device LLR buffer back as float64 (B, n) (tests of the generator). */
 int qcl_state_get_llr(qcl_state *st, double *llr);
+/* Lanes per group (W) of the state's layout, and whether its decodes run on the flow
+ * engine (FP32 or FP16 messages, row degree <= 12, W >= 4, tables fit in shared memory);
+ * the frame pool (qcl_state_decode_pool) and FP16 messages need it. */
+int qcl_state_info(qcl_state *st, int32_t *lanes, int32_t *flow_engine);
 /* Device-time breakdown of the last qcl_state_decode: number of layer-kernel launches and
  * their summed CUDA-event time (ms); used by bench.py's roofline. */
 int qcl_state_kernel_stats(qcl_state *st, int64_t *layer_launches, float *layer_ms, int64_t *all_launches);
@@ -146,10 +150,13 @@ int qcl_state_set_engine(qcl_state *st, int32_t engine);
 
 /* ---- asynchronous path (streaming / overlapped host<->device copies) ---------------
  * Everything below only enqueues work on the state's stream; qcl_state_wait blocks until
- * the results requested by qcl_state_results_async have landed.  Host buffers should be
- * pinned (qcl_host_alloc) for the copies to overlap device work.
+ * the results requested by qcl_state_results_async have landed.  Result buffers should
+ * be pinned (qcl_host_alloc) for the copies to overlap device work; pageable LLR inputs
+ * are converted and staged through pinned chunks by host threads before the call returns
+ * (the caller may reuse them at once), pinned ones are read asynchronously.
  * qcl_state_set_syndrome_hint: the caller states whether the (B, m) target is nonzero
- * (nonzero = 0 or syndrome = NULL: all-zero target, nothing is copied).
+ * (nonzero = 0 or syndrome = NULL: all-zero target, nothing is copied; nonzero < 0: the
+ * library checks on the host threads).
  * qcl_state_decode_async: the decode of qcl_state_decode without host synchronisation;
  * with early termination every layer launch after the last convergence returns at once. */
 int qcl_state_set_syndrome_hint(qcl_state *st, const uint8_t *syndrome, int32_t nonzero);

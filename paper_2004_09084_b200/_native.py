@@ -63,6 +63,7 @@ _SIGNATURES = {
     "qcl_state_truths": ([_vp, _vp], ctypes.c_int),
     "qcl_state_get_llr": ([_vp, _vp], ctypes.c_int),
     "qcl_state_kernel_stats": ([_vp, _vp, _vp, _vp], ctypes.c_int),
+    "qcl_state_info": ([_vp, _vp, _vp], ctypes.c_int),
     "qcl_state_set_engine": ([_vp, _i32], ctypes.c_int),
     "qcl_state_frame_errors": ([_vp, _vp], ctypes.c_int),
     "qcl_state_decode_pool": ([_vp, _vp, ctypes.c_uint64, _i64, _i64, _i64, _dbl, _vp, _vp, _vp, _vp], ctypes.c_int),
@@ -273,15 +274,22 @@ class State:
         call("qcl_state_kernel_stats", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
         return int(a.value), float(b.value), int(c.value)
 
+    def info(self):
+        """(lanes per group, decodes run on the flow engine)"""
+        w, f = ctypes.c_int32(), ctypes.c_int32()
+        call("qcl_state_info", self.handle, ctypes.byref(w), ctypes.byref(f))
+        return int(w.value), bool(f.value)
+
     def set_engine(self, engine):
         call("qcl_state_set_engine", self.handle, int(engine))
 
     # asynchronous path
-    def set_syndrome_hint(self, syndrome, nonzero):
-        if syndrome is None or not nonzero:
+    def set_syndrome_hint(self, syndrome, nonzero=None):
+        """nonzero None: the library checks for an all-zero target on its host threads."""
+        if syndrome is None or (nonzero is not None and not nonzero):
             call("qcl_state_set_syndrome_hint", self.handle, None, 0)
             return
-        call("qcl_state_set_syndrome_hint", self.handle, ptr(syndrome), 1)
+        call("qcl_state_set_syndrome_hint", self.handle, ptr(syndrome), -1 if nonzero is None else 1)
 
     def decode_async(self, qcfg):
         call("qcl_state_decode_async", self.handle, ctypes.byref(qcfg))
@@ -295,24 +303,35 @@ class State:
         return float(ms.value)
 
 
+class _PinnedBlock:
+    """Owns one qcl_host_alloc block; freed when the last array viewing it is gone."""
+
+    def __init__(self, nbytes):
+        p = ctypes.c_void_p()
+        call("qcl_host_alloc", max(nbytes, 1), ctypes.byref(p))
+        self.ptr = p
+
+    def __del__(self):
+        p = getattr(self, "ptr", None)
+        if p and p.value and _lib is not None and not sys.is_finalizing():
+            _lib.qcl_host_free(p)
+            self.ptr = None
+
+
 class PinnedArray:
-    """Page-locked host memory (``qcl_host_alloc``) viewed as a numpy array."""
+    """Page-locked host memory (``qcl_host_alloc``) viewed as a numpy array.
+
+    The memory block is owned by the array's buffer object, so every numpy view of it
+    (for example a result yielded by ``decode_stream``) keeps it alive even after this
+    wrapper is dropped."""
 
     def __init__(self, shape, dtype):
         dtype = np.dtype(dtype)
         nbytes = int(np.prod(shape)) * dtype.itemsize
-        p = ctypes.c_void_p()
-        call("qcl_host_alloc", max(nbytes, 1), ctypes.byref(p))
-        self._ptr = p
-        buf = (ctypes.c_uint8 * max(nbytes, 1)).from_address(p.value)
+        block = _PinnedBlock(nbytes)
+        buf = (ctypes.c_uint8 * max(nbytes, 1)).from_address(block.ptr.value)
+        buf._owner = block  # the buffer (the base of every view) keeps the block alive
         self.array = np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dtype).reshape(shape)
-
-    def __del__(self):
-        p = getattr(self, "_ptr", None)
-        if p and p.value and _lib is not None and not sys.is_finalizing():
-            self.array = None
-            _lib.qcl_host_free(p)
-            self._ptr = None
 
 
 def decode_arrays(plan, qcfg, llr, syndrome):

@@ -155,6 +155,9 @@ class CampaignCell:
 class CampaignReport:
     cells: tuple
     metadata: dict = field(default_factory=dict)
+    # per cell, beside the reference's 8 columns (JSON only): the HBM
+    # roofline of the decode at that point (see _roofline)
+    roofline: tuple = ()
 
 
 @dataclass(frozen=True)
@@ -319,13 +322,23 @@ def _uses_pool(cfg):
 class _PoolRunner(_DeviceChannelRunner):
     """All frames of an SNR point through ``batch_size`` lanes per GPU (frame pool)."""
 
-    def point(self, snr_idx, chan, frames):
+    def _jobs(self, snr_idx, snr, frames):
         sizes = [len(c) for c in np.array_split(np.arange(frames), len(self.plans))]
         jobs, first = [], 0
         for dev, size in enumerate(sizes):
             if size:
-                jobs.append((dev, snr_idx, chan.snr, first, size))
+                jobs.append((dev, snr_idx, snr, first, size))
             first += size
+        return jobs
+
+    def supported(self, frames):
+        """The pool needs the flow engine for every per-GPU lane set (>= 4 lanes, row
+        degree <= 12, tables in shared memory): asked of the engine itself."""
+        return all(self._state(dev, min(self.cfg.batch_size, count)).info()[1]
+                   for dev, _, _, _, count in self._jobs(0, 1.0, frames))
+
+    def point(self, snr_idx, chan, frames):
+        jobs = self._jobs(snr_idx, chan.snr, frames)
 
         def run(job):
             dev, si, snr, f0, count = job
@@ -337,6 +350,58 @@ class _PoolRunner(_DeviceChannelRunner):
         parts = list(self.pool.map(run, jobs)) if self.pool else [run(j) for j in jobs]
         return (np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]),
                 np.concatenate([p[2] for p in parts]), max(p[3] for p in parts))
+
+
+BYTES_PER_EDGE_ITERATION = {"fp32": 16, "fp64": 32, "fp32-msg16": 12}
+
+
+def _hbm_peak():
+    """Per-GPU HBM bandwidth the fractions refer to: MEASURED_PEAKS.json (driver-written,
+    next to the package) when present, else the B200 profiling recipe's fallback."""
+    try:
+        peaks = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())
+        return float(peaks["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _device_metadata(cfg, pool):
+    import os
+
+    peak, source = _hbm_peak()
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        cores = os.cpu_count()
+    return {
+        "precision": cfg.precision,
+        "channel": cfg.channel,
+        "devices": list(cfg.devices),
+        "gpu_count": len(set(cfg.devices)),
+        "host_cores": cores,
+        "frame_pool": bool(pool),
+        "bytes_per_edge_iteration": BYTES_PER_EDGE_ITERATION[cfg.precision],
+        "hbm_peak_gbs_per_gpu": peak,
+        "hbm_peak_source": source,
+    }
+
+
+def _roofline(cell, iterations_total, wall, device_meta):
+    """Algorithmic HBM bytes of the decode at one SNR point (bytes per edge-iteration x
+    expanded edges x iterations executed, summed over frames) over its decode wall time,
+    per GPU and as a fraction of the per-GPU peak."""
+    bpe = device_meta["bytes_per_edge_iteration"]
+    edge_iterations = int(iterations_total) * int(cell.total_expanded_edges)
+    achieved = bpe * edge_iterations / wall / 1e9 if wall > 0 else 0.0
+    per_gpu = achieved / max(1, device_meta["gpu_count"])
+    return {
+        "snr": cell.snr,
+        "edge_iterations": edge_iterations,
+        "achieved_gbs": achieved,
+        "achieved_gbs_per_gpu": per_gpu,
+        "roofline_fraction": per_gpu / device_meta["hbm_peak_gbs_per_gpu"],
+        "bytes_per_edge_iteration": bpe,
+    }
 
 
 def run_campaign(cfg):
@@ -355,8 +420,10 @@ def run_campaign(cfg):
     pool = _uses_pool(cfg)
     runner_cls = _PoolRunner if pool else (_HostChannelRunner if cfg.channel == "host" else _DeviceChannelRunner)
     runner = runner_cls(cfg, index, schedule, dcfg, n, m, rows)
+    if pool and not runner.supported(frames):
+        pool = False  # the batched device-channel decode (a _PoolRunner is one) runs instead
 
-    cells = []
+    cells, roofline = [], []
     try:
         for snr_idx, snr in enumerate(cfg.snr_list):
             chan = ChannelConfig(snr=snr, seed=cfg.seed)
@@ -386,10 +453,14 @@ def run_campaign(cfg):
                     utilization=util.utilization,
                 )
             )
+            roofline.append((iterations_total, wall))
     finally:
         runner.close()
 
-    return CampaignReport(cells=tuple(cells), metadata=_campaign_metadata(cfg, base, desc, schedule))
+    metadata = _campaign_metadata(cfg, base, desc, schedule)
+    metadata["device"] = _device_metadata(cfg, pool)
+    return CampaignReport(cells=tuple(cells), metadata=metadata,
+                          roofline=tuple(_roofline(c, it, w, metadata["device"]) for c, (it, w) in zip(cells, roofline)))
 
 
 def compare_schedules(cfg):
@@ -413,11 +484,14 @@ def report_to_dict(report):
             "single_layer_count": report.single_layer_count,
             "merged_layer_count": report.merged_layer_count,
         }
-    return {
+    out = {
         "schema_version": SCHEMA_VERSION,
         "metadata": report.metadata,
         "cells": [asdict(cell) for cell in report.cells],
     }
+    if report.roofline:
+        out["roofline"] = list(report.roofline)
+    return out
 
 
 def emit_report(report, fmt, path):

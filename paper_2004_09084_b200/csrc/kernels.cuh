@@ -841,25 +841,27 @@ __global__ void synth_llr_kernel(int64_t B, int64_t Bp, int64_t n, int lw, uint6
 // frame b differs anywhere from its transmitted word (all-zero when truths == nullptr).
 // blockIdx.y = frame; 16-byte vector compares when n is a multiple of 16.
 __global__ void __launch_bounds__(kBlock) frame_mismatch_kernel(const uint8_t *words, const uint8_t *truths,
-                                                                int64_t n, uint8_t *mismatch) {
-    const int64_t b = blockIdx.y;
-    const uint8_t *w = words + b * n;
-    const uint8_t *t = truths ? truths + b * n : nullptr;
-    bool bad = false;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    if ((n & 15) == 0) {
-        const uint4 *w4 = reinterpret_cast<const uint4 *>(w);
-        const uint4 *t4 = reinterpret_cast<const uint4 *>(t);
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 16; i += stride) {
-            const uint4 x = __ldg(w4 + i);
-            const uint4 y = t ? __ldg(t4 + i) : make_uint4(0, 0, 0, 0);
-            bad |= ((x.x ^ y.x) | (x.y ^ y.y) | (x.z ^ y.z) | (x.w ^ y.w)) != 0;
+                                                                int64_t n, int64_t B, uint8_t *mismatch) {
+    // frames grid-stride along y (gridDim.y is capped at 65535)
+    for (int64_t b = blockIdx.y; b < B; b += gridDim.y) {
+        const uint8_t *w = words + b * n;
+        const uint8_t *t = truths ? truths + b * n : nullptr;
+        bool bad = false;
+        const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+        if ((n & 15) == 0) {
+            const uint4 *w4 = reinterpret_cast<const uint4 *>(w);
+            const uint4 *t4 = reinterpret_cast<const uint4 *>(t);
+            for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n / 16; i += stride) {
+                const uint4 x = __ldg(w4 + i);
+                const uint4 y = t ? __ldg(t4 + i) : make_uint4(0, 0, 0, 0);
+                bad |= ((x.x ^ y.x) | (x.y ^ y.y) | (x.z ^ y.z) | (x.w ^ y.w)) != 0;
+            }
+        } else {
+            for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+                bad |= w[i] != (t ? t[i] : 0);
         }
-    } else {
-        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-            bad |= w[i] != (t ? t[i] : 0);
+        if (__syncthreads_or(bad) && threadIdx.x == 0) mismatch[b] = 1;
     }
-    if (__syncthreads_or(bad) && threadIdx.x == 0) mismatch[b] = 1;
 }
 
 // ---- frame pool (qcl_state_decode_pool): lanes refilled as their frames finish --------

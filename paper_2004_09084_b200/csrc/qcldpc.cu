@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 #include "pipeline.cuh"
 #include "flow.cuh"
+#include "hostio.h"
 
 using namespace qcl;
 
@@ -46,6 +47,26 @@ static int fail(int code, const char *fmt, ...) {
     } while (0)
 
 static int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Every entry point runs on its plan's device and gives the calling thread its current
+// device back on return (callers such as torch rely on it).
+struct DeviceScope {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceScope(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        ok = prev == dev || cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceScope() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DeviceScope(const DeviceScope &) = delete;
+    DeviceScope &operator=(const DeviceScope &) = delete;
+};
+#define DEVICE_SCOPE(dev)                                                           \
+    DeviceScope dscope_(dev);                                                       \
+    if (!dscope_.ok) return fail(QCL_ECUDA, "cudaSetDevice(%d) failed", (int)(dev))
 
 // FP32 bound on |r|: Phi(eps) (the reference clamps `others` to >= eps, decoder.py:104),
 // and the clip where it binds (decoder.py:244-245).
@@ -140,6 +161,7 @@ struct qcl_state {
     int32_t *prefill = nullptr;    // [Bp] lanes to refill this sweep
     int32_t *pcount = nullptr;     // [0] refills this sweep, [1] frames handed out
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sweep_events;
+    HostRing ring;  // pinned chunks of the pageable-memory copy pipelines (hostio.h)
 };
 
 // ----------------------------------------------------------------------------- dispatch
@@ -811,7 +833,8 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
             }
         }
     }
-    cudaError_t e = cudaSetDevice(device);
+    DeviceScope dscope_(device);
+    cudaError_t e = dscope_.ok ? cudaSuccess : cudaErrorInvalidDevice;
     if (e == cudaSuccess) e = cudaMalloc(&p->fedge_tab, sizeof(uint2) * n_edges);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->fedge_tab, h_etab.data(), sizeof(uint2) * n_edges, cudaMemcpyHostToDevice);
@@ -845,7 +868,7 @@ int qcl_state_destroy(qcl_state *st);
 
 int qcl_plan_destroy(qcl_plan *p) {
     if (!p) return QCL_OK;
-    cudaSetDevice(p->device);
+    DeviceScope dscope_(p->device);
     for (auto *s : p->cache) qcl_state_destroy(s);
     cudaFree(p->slots);
     cudaFree(p->edges);
@@ -883,7 +906,7 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
     if (batch < 1) return fail(QCL_EVALUE, "batch must be at least 1");
     if (precision != QCL_PREC_FP32 && precision != QCL_PREC_FP64 && precision != QCL_PREC_FP32_MSG16)
         return fail(QCL_EVALUE, "unknown precision %d", precision);
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     auto st = new qcl_state();
     st->plan = p;
     st->B = batch;
@@ -943,7 +966,7 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
 
 int qcl_state_destroy(qcl_state *st) {
     if (!st) return QCL_OK;
-    cudaSetDevice(st->plan->device);
+    DeviceScope dscope_(st->plan->device);
     if (st->stream) cudaStreamSynchronize(st->stream);
     if (st->fstats) {
         unsigned long long h[16] = {};
@@ -975,6 +998,7 @@ int qcl_state_destroy(qcl_state *st) {
     if (st->ev1) cudaEventDestroy(st->ev1);
     if (st->ev_done) cudaEventDestroy(st->ev_done);
     if (st->staging2) cudaFree(st->staging2);
+    st->ring.release();
     if (st->stream) cudaStreamDestroy(st->stream);
     for (int i = 0; i < kSideStreams; i++) {
         if (st->side[i]) cudaStreamDestroy(st->side[i]);
@@ -1008,15 +1032,37 @@ static int ensure_staging2(qcl_state *st, size_t bytes) {
 int qcl_state_set_llr(qcl_state *st, const void *llr0, int32_t dtype) {
     if (!st || !llr0) return fail(QCL_EVALUE, "NULL argument");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     const size_t sz = dtype == QCL_DTYPE_F64 ? 8 : 4;
     if (dtype != QCL_DTYPE_F64 && dtype != QCL_DTYPE_F32) return fail(QCL_EVALUE, "unknown llr dtype");
     const size_t bytes = (size_t)st->B * p->n * sz;
+    const int64_t total = st->Bp * p->n;
+    const unsigned grid = (unsigned)cdiv(total, kBlock);
+    if (!host_is_pinned(llr0)) {
+        // pageable caller memory (the reference's float64 arrays): convert to the state's
+        // type on the host threads while the copy engine moves the previous chunk
+        const int64_t cnt = st->B * p->n;
+        int rc = ensure_staging(st, (size_t)cnt * st->esz);
+        if (rc) return rc;
+        if (st->prec == QCL_PREC_FP32) {
+            CK(dtype == QCL_DTYPE_F64
+                   ? upload_converted(st->ring, (float *)st->staging, (const double *)llr0, cnt, st->stream)
+                   : upload_converted(st->ring, (float *)st->staging, (const float *)llr0, cnt, st->stream));
+            llr_to_lanes_kernel<float, float><<<grid, kBlock, 0, st->stream>>>(
+                (const float *)st->staging, st->B, st->Bp, p->n, st->lw, (float *)st->llr);
+        } else {
+            CK(dtype == QCL_DTYPE_F64
+                   ? upload_converted(st->ring, (double *)st->staging, (const double *)llr0, cnt, st->stream)
+                   : upload_converted(st->ring, (double *)st->staging, (const float *)llr0, cnt, st->stream));
+            llr_to_lanes_kernel<double, double><<<grid, kBlock, 0, st->stream>>>(
+                (const double *)st->staging, st->B, st->Bp, p->n, st->lw, (double *)st->llr);
+        }
+        CK(cudaGetLastError());
+        return QCL_OK;
+    }
     int rc = ensure_staging(st, bytes);
     if (rc) return rc;
     CK(cudaMemcpyAsync(st->staging, llr0, bytes, cudaMemcpyHostToDevice, st->stream));
-    const int64_t total = st->Bp * p->n;
-    const unsigned grid = (unsigned)cdiv(total, kBlock);
     if (st->prec == QCL_PREC_FP32) {
         if (dtype == QCL_DTYPE_F64)
             llr_to_lanes_kernel<float, double><<<grid, kBlock, 0, st->stream>>>(
@@ -1041,7 +1087,7 @@ int qcl_state_set_llr_synthetic(qcl_state *st, uint64_t seed, int64_t snr_idx, i
     if (!st) return fail(QCL_EVALUE, "NULL argument");
     if (!(snr > 0)) return fail(QCL_EVALUE, "snr must be positive");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     if (encode_mode && !st->truths) CK(cudaMalloc(&st->truths, (size_t)st->B * p->n));
     const double sigma2 = 1.0 / snr, sigma = sqrt(sigma2);
     const int64_t total = st->Bp * cdiv(p->n, 4);
@@ -1073,7 +1119,7 @@ int qcl_state_set_llr_synthetic(qcl_state *st, uint64_t seed, int64_t snr_idx, i
 
 int qcl_state_truths(qcl_state *st, uint8_t *words) {
     if (!st || !words) return fail(QCL_EVALUE, "NULL argument");
-    CK(cudaSetDevice(st->plan->device));
+    DEVICE_SCOPE(st->plan->device);
     if (!st->truths || !st->truths_valid) {
         CK(cudaStreamSynchronize(st->stream));
         memset(words, 0, (size_t)st->B * st->plan->n);
@@ -1087,12 +1133,12 @@ int qcl_state_truths(qcl_state *st, uint8_t *words) {
 int qcl_state_frame_errors(qcl_state *st, uint8_t *mismatch) {
     if (!st || !mismatch) return fail(QCL_EVALUE, "NULL argument");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     CK(cudaMemsetAsync(st->take, 0, st->B, st->stream));  // reused as the per-frame flag buffer
     const int64_t units = (p->n % 16 == 0) ? p->n / 16 : p->n;
     const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(units, kBlock), 64));
-    frame_mismatch_kernel<<<dim3(gx, (unsigned)st->B), kBlock, 0, st->stream>>>(
-        st->words, st->truths_valid ? st->truths : nullptr, p->n, st->take);
+    frame_mismatch_kernel<<<dim3(gx, (unsigned)std::min<int64_t>(st->B, 65535)), kBlock, 0, st->stream>>>(
+        st->words, st->truths_valid ? st->truths : nullptr, p->n, st->B, st->take);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(mismatch, st->take, st->B, cudaMemcpyDeviceToHost, st->stream));
     CK(cudaStreamSynchronize(st->stream));
@@ -1102,7 +1148,7 @@ int qcl_state_frame_errors(qcl_state *st, uint8_t *mismatch) {
 int qcl_state_get_llr(qcl_state *st, double *llr) {
     if (!st || !llr) return fail(QCL_EVALUE, "NULL argument");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     int rc = ensure_staging(st, (size_t)st->B * p->n * 8);
     if (rc) return rc;
     const int64_t total = st->B * p->n;
@@ -1122,27 +1168,32 @@ int qcl_state_get_llr(qcl_state *st, double *llr) {
 int qcl_state_set_syndrome(qcl_state *st, const uint8_t *syndrome) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     if (!syndrome) {
         st->has_syn = false;
         return QCL_OK;
     }
     const size_t bytes = (size_t)st->B * p->m;
+    // an all-zero target (the campaign default, bench.py:227-228) is detected on the host
+    // and never uploaded: it takes the syndrome-free kernel variant, which does not read
+    // the per-check syndrome bytes at all
+    if (!host_any_nonzero(syndrome, (int64_t)bytes)) {
+        st->has_syn = false;
+        return QCL_OK;
+    }
     int rc = ensure_staging(st, bytes);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(st->staging, syndrome, bytes, cudaMemcpyHostToDevice, st->stream));
+    if (host_is_pinned(syndrome))
+        CK(cudaMemcpyAsync(st->staging, syndrome, bytes, cudaMemcpyHostToDevice, st->stream));
+    else
+        CK(upload_converted(st->ring, (uint8_t *)st->staging, syndrome, (int64_t)bytes, st->stream));
     CK(cudaMemsetAsync(st->n_active, 0, sizeof(int), st->stream));
     const int64_t total = st->Bp * p->m;
     syndrome_to_lanes_kernel<<<(unsigned)cdiv(total, kBlock), kBlock, 0, st->stream>>>(
         (const uint8_t *)st->staging, p->slots, st->B, st->Bp, p->S, p->z, st->lw, st->syn, st->n_active);
     CK(cudaGetLastError());
-    // an all-zero target (the campaign default, bench.py:227-228) takes the syndrome-free
-    // kernel variant, which does not read the per-check syndrome bytes at all
-    CK(cudaMemcpyAsync(st->h_n_active, st->n_active, sizeof(int), cudaMemcpyDeviceToHost, st->stream));
-    CK(cudaStreamSynchronize(st->stream));
-    st->has_syn = *st->h_n_active != 0;
-    if (st->has_syn) return enqueue_syn_pack(st);
-    return QCL_OK;
+    st->has_syn = true;
+    return enqueue_syn_pack(st);
 }
 
 // new_state (decoder.py:191-202): L = clip(llr), R = 0.  zero_r = false when the first
@@ -1166,14 +1217,14 @@ static int enqueue_reset(qcl_state *st, double clip, bool zero_r = true) {
 int qcl_state_reset(qcl_state *st, double llr_clip) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
     if (!(llr_clip > 0)) return fail(QCL_EVALUE, "llr_clip must be positive");
-    CK(cudaSetDevice(st->plan->device));
+    DEVICE_SCOPE(st->plan->device);
     return enqueue_reset(st, llr_clip);
 }
 
 int qcl_state_upload(qcl_state *st, const double *posterior, const double *messages) {
     if (!st || !posterior) return fail(QCL_EVALUE, "NULL argument");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     const int64_t Ez = (int64_t)p->E * p->z;
     const size_t pb = (size_t)st->B * p->n * 8, mb = (size_t)st->B * Ez * 8;
     int rc = ensure_staging(st, pb + mb);
@@ -1201,7 +1252,7 @@ int qcl_state_upload(qcl_state *st, const double *posterior, const double *messa
 int qcl_state_download(qcl_state *st, double *posterior, double *messages) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     const int64_t Ez = (int64_t)p->E * p->z;
     const size_t pb = (size_t)st->B * p->n * 8, mb = (size_t)st->B * Ez * 8;
     int rc = ensure_staging(st, pb + mb);
@@ -1230,7 +1281,7 @@ int qcl_state_layers(qcl_state *st, int32_t first, int32_t count, double llr_cli
     const qcl_plan *p = st->plan;
     if (first < 0 || count < 0 || first + count > p->n_layers)
         return fail(QCL_EVALUE, "layer range [%d, %d) outside [0, %d)", first, first + count, p->n_layers);
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     if (st->msg16) {
         if (!use_flow(st) || first != 0 || count != p->n_layers) return msg16_unsupported(st, "whole sweeps only");
         int rc = ensure_flow(st, 1);
@@ -1263,7 +1314,7 @@ int qcl_state_layers(qcl_state *st, int32_t first, int32_t count, double llr_cli
 
 int qcl_state_hard_decision(qcl_state *st, uint8_t *words) {
     if (!st || !words) return fail(QCL_EVALUE, "NULL argument");
-    CK(cudaSetDevice(st->plan->device));
+    DEVICE_SCOPE(st->plan->device);
     int rc = enqueue_signs(st);
     if (!rc) rc = enqueue_words(st, nullptr);
     if (rc) return rc;
@@ -1274,7 +1325,7 @@ int qcl_state_hard_decision(qcl_state *st, uint8_t *words) {
 
 int qcl_state_syndrome_ok(qcl_state *st, uint8_t *ok) {
     if (!st || !ok) return fail(QCL_EVALUE, "NULL argument");
-    CK(cudaSetDevice(st->plan->device));
+    DEVICE_SCOPE(st->plan->device);
     int rc = enqueue_check(st);
     if (rc) return rc;
     std::vector<uint32_t> un(st->G);
@@ -1360,7 +1411,7 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     if (rc) return rc;
     if (cfg->precision != st->api_prec) return fail(QCL_EVALUE, "config precision differs from the state's");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     st->launches_layer = st->launches_all = 0;
     st->layer_ms = 0;
     const bool et = cfg->early_termination != 0;
@@ -1498,7 +1549,7 @@ int qcl_state_decode_pool(qcl_state *st, const qcl_config *cfg, uint64_t seed, i
     if (!(snr > 0)) return fail(QCL_EVALUE, "snr must be positive");
     if (!use_flow(st)) return fail(QCL_EUNSUP, "the frame pool runs on the flow engine (FP32, engine 4)");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     if ((rc = ensure_flow(st, 2))) return rc;
     if (!use_flow(st)) return fail(QCL_EUNSUP, "the frame pool runs on the flow engine (FP32, engine 4)");
     auto al = [&](void **ptr, size_t bytes) -> int {
@@ -1624,7 +1675,7 @@ int qcl_state_decode_async(qcl_state *st, const qcl_config *cfg) {
 int qcl_state_results_async(qcl_state *st, uint8_t *words, uint8_t *converged, int64_t *iterations) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
     if (words) CK(cudaMemcpyAsync(words, st->words, (size_t)st->B * p->n, cudaMemcpyDeviceToHost, st->stream));
     if (converged) CK(cudaMemcpyAsync(converged, st->conv, st->B, cudaMemcpyDeviceToHost, st->stream));
     if (iterations)
@@ -1635,7 +1686,7 @@ int qcl_state_results_async(qcl_state *st, uint8_t *words, uint8_t *converged, i
 
 int qcl_state_wait(qcl_state *st, float *decode_ms) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
-    CK(cudaSetDevice(st->plan->device));
+    DEVICE_SCOPE(st->plan->device);
     CK(cudaEventSynchronize(st->ev_done));
     return finish_decode(st, decode_ms);
 }
@@ -1643,15 +1694,20 @@ int qcl_state_wait(qcl_state *st, float *decode_ms) {
 int qcl_state_set_syndrome_hint(qcl_state *st, const uint8_t *syndrome, int32_t nonzero) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
+    DEVICE_SCOPE(p->device);
+    const size_t bytes = (size_t)st->B * p->m;
+    // nonzero < 0: the caller did not look; the host threads check for an all-zero target
+    if (syndrome && nonzero < 0) nonzero = host_any_nonzero(syndrome, (int64_t)bytes);
     if (!syndrome || !nonzero) {
         st->has_syn = false;
         return QCL_OK;
     }
-    const size_t bytes = (size_t)st->B * p->m;
     int rc = ensure_staging2(st, bytes);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(st->staging2, syndrome, bytes, cudaMemcpyHostToDevice, st->stream));
+    if (host_is_pinned(syndrome))
+        CK(cudaMemcpyAsync(st->staging2, syndrome, bytes, cudaMemcpyHostToDevice, st->stream));
+    else
+        CK(upload_converted(st->ring, (uint8_t *)st->staging2, syndrome, (int64_t)bytes, st->stream));
     const int64_t total = st->Bp * p->m;
     syndrome_to_lanes_kernel<<<(unsigned)cdiv(total, kBlock), kBlock, 0, st->stream>>>(
         (const uint8_t *)st->staging2, p->slots, st->B, st->Bp, p->S, p->z, st->lw, st->syn, st->n_active);
@@ -1674,12 +1730,33 @@ int qcl_host_free(void *ptr) {
 int qcl_state_results(qcl_state *st, uint8_t *words, uint8_t *converged, int64_t *iterations) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
     const qcl_plan *p = st->plan;
-    CK(cudaSetDevice(p->device));
-    if (words) CK(cudaMemcpyAsync(words, st->words, (size_t)st->B * p->n, cudaMemcpyDeviceToHost, st->stream));
+    DEVICE_SCOPE(p->device);
+    if (words && !host_is_pinned(words))  // pageable: pipelined through the pinned ring
+        CK(download_bytes(st->ring, words, st->words, (int64_t)st->B * p->n, st->stream));
+    else if (words)
+        CK(cudaMemcpyAsync(words, st->words, (size_t)st->B * p->n, cudaMemcpyDeviceToHost, st->stream));
     if (converged) CK(cudaMemcpyAsync(converged, st->conv, st->B, cudaMemcpyDeviceToHost, st->stream));
     if (iterations)
         CK(cudaMemcpyAsync(iterations, st->iters, st->B * sizeof(int64_t), cudaMemcpyDeviceToHost, st->stream));
     CK(cudaStreamSynchronize(st->stream));
+    return QCL_OK;
+}
+
+int qcl_state_info(qcl_state *st, int32_t *lanes, int32_t *flow_engine) {
+    if (!st) return fail(QCL_EVALUE, "NULL argument");
+    DEVICE_SCOPE(st->plan->device);
+    if (lanes) *lanes = st->W;
+    if (flow_engine) {
+        // the static conditions first; then the tiling, whose shared-memory fit decides the rest
+        bool ok = st->engine == 4 && st->prec == QCL_PREC_FP32 && st->plan->flow_ok && st->plan->max_degree <= 12 &&
+                  st->W >= 4;
+        if (ok) {
+            int rc = ensure_flow(st, 1);
+            if (rc) return rc;
+            ok = use_flow(st);
+        }
+        *flow_engine = ok ? 1 : 0;
+    }
     return QCL_OK;
 }
 
@@ -1757,7 +1834,7 @@ int qcl_phi(const double *x, int64_t n, double phi_epsilon, double llr_clip, int
             double *out) {
     if (n < 0 || (n > 0 && (!x || !out))) return fail(QCL_EVALUE, "NULL argument");
     if (n == 0) return QCL_OK;
-    CK(cudaSetDevice(device));
+    DEVICE_SCOPE(device);
     double *d = nullptr;
     CK(cudaMalloc(&d, 2 * n * sizeof(double)));
     cudaError_t e = cudaMemcpy(d, x, n * sizeof(double), cudaMemcpyHostToDevice);

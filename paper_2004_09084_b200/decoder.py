@@ -263,10 +263,12 @@ def _stream_decode(self, batches, depth=2, copy=False):
     host<->device copies of one batch overlap the decoding of the next.
 
     ``depth`` device workspaces are cycled (each ~1.5 GB for 64 codewords of the n=10^6
-    code).  Inputs are read asynchronously: pinned arrays (``_native.PinnedArray``) copy
-    at full PCIe speed, and every input must stay unmodified until its result is yielded.
-    Yielded arrays are views of pinned buffers that are reused ``depth`` batches later
-    unless ``copy=True``.
+    code).  Pageable inputs (the reference's float64 arrays) are converted and staged
+    into pinned chunks by the library's host threads before ``set_llr`` returns, while
+    the previous batch decodes; pinned float32 arrays (``_native.PinnedArray``) are read
+    asynchronously and must stay unmodified until their result is yielded.  Yielded
+    arrays are views of pinned buffers (kept alive by the views) that are overwritten
+    ``depth`` batches later unless ``copy=True``.
     """
     # workspaces persist across calls (per host thread): their whole-decode CUDA graphs
     # are instantiated once
@@ -302,7 +304,7 @@ def _stream_decode(self, batches, depth=2, copy=False):
         st = slot.state
         slot.inputs = (llr, syn)
         st.set_llr(llr)
-        st.set_syndrome_hint(syn, bool(syn.any()))
+        st.set_syndrome_hint(syn)  # all-zero check on the library's host threads
         st.decode_async(self._qcfg)
         st.results_async(slot.words.array, slot.conv.array, slot.iters.array)
         pending.append(slot)

@@ -175,10 +175,30 @@ inline void flow_sweep_divisor(uint32_t d, uint32_t &mul, uint32_t &shift) {
     shift = l;
 }
 
-__device__ __forceinline__ int ld_relaxed(const int *p) {
+// QCL_FLOW_ACQUIRE: how a tile's dependency polls acquire the storers' releases.
+//   0 (default): relaxed polls; the ordering rests on an sm_100 property, see spin_until;
+//   1: ld.acquire.gpu on every flag load (a PTX-model synchronizes-with edge): +4.8% per
+//      decode in bursts, +5.8% sustained (tools/flow_sustained.py, DESIGN 3.1);
+//   2: relaxed polls, then one fence.acq_rel.gpu per resolved tile: +12%.
+#ifndef QCL_FLOW_ACQUIRE
+#define QCL_FLOW_ACQUIRE 0
+#endif
+#if QCL_FLOW_ACQUIRE == 0 && defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 900 || __CUDA_ARCH__ >= 1100)
+#error "relaxed flag polls are argued for sm_90..sm_10x bulk-copy semantics only; build with -DQCL_FLOW_ACQUIRE=1"
+#endif
+__device__ __forceinline__ int ld_flag(const int *p) {
     int v;
+#if QCL_FLOW_ACQUIRE == 1
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#else
     asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#endif
     return v;
+}
+__device__ __forceinline__ void flow_acquire_fence() {
+#if QCL_FLOW_ACQUIRE == 2
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
 }
 __device__ __forceinline__ void st_release(int *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -186,15 +206,27 @@ __device__ __forceinline__ void st_release(int *p, int v) {
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-// Poll a tile flag.  Relaxed loads go to L2 (the point of coherence the storer released
-// the flag to, after its bulk writes completed); the bulk copies issued after the poll
-// loop exits are control dependent on the observed value and also read L2, and the
-// fence.proxy.async that follows orders them after the poll.  No gpu-scope acquire
-// fence: it would cost a MEMBAR.ALL.GPU plus an L1 invalidation per tile.
+// Poll a tile flag.  Storer side (every variant): the tile's bulk writes complete
+// (cp.async.bulk.wait_group 0: the writes are performed, i.e. in L2, the point of
+// coherence for the async proxy) -> fence.proxy.async.global -> st.release.gpu of the
+// flag.  Reader side:
+//   QCL_FLOW_ACQUIRE = 1: the scheduler's ld.acquire.gpu that observes the flag
+//   synchronizes with that release; its mbarrier arrive (release, CTA) -> the loader's
+//   mbarrier wait (acquire, CTA) carries it to the loader (causality order is
+//   transitive), whose fence.proxy.async.global orders its bulk reads after it.
+//   QCL_FLOW_ACQUIRE = 0 (default): the same chain with a relaxed observing load.  The
+//   PTX model gives no synchronizes-with edge for it; what makes it correct here is that
+//   (a) the loader's bulk reads cannot be issued before the observation (they are data-
+//   and control-dependent on the header the scheduler publishes after the poll returns),
+//   and (b) cp.async.bulk reads are served by L2, where the released bytes already are
+//   (no L1 copy can be stale for the async proxy).  That is an sm_90/sm_100 property,
+//   hence the #error above for other architectures.  Measured cost of the formal
+//   variant: +4.8% in bursts, +5.8% sustained; checked by tools/flow_stress.py (repeated
+//   decodes bit-identical to the per-layer engine) and the bit-exact engine tests.
 __device__ __forceinline__ int spin_until(const int *flag, int need) {
-    if (ld_relaxed(flag) >= need) return 0;
+    if (ld_flag(flag) >= need) return 0;
     int polls = 1;
-    while (ld_relaxed(flag) < need) {
+    while (ld_flag(flag) < need) {
         __nanosleep(64);
         polls++;
     }
@@ -636,12 +668,13 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                     flag_plan(h, fl, need, lo, nlo, nfl);
 #pragma unroll
                     for (int m = 0; m < 4; m++)
-                        if (m < nfl) fv[m] = ld_relaxed(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE);
+                        if (m < nfl) fv[m] = ld_flag(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE);
 #pragma unroll
                     for (int m = 0; m < 4; m++)
                         if (m < nfl && fv[m] < need) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need);
                     for (int m = 4; m < nfl; m++) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need);
                 }
+                flow_acquire_fence();
                 FLOW_TICK(2);
                 if (prof) {
                     polls = __reduce_add_sync(0xffffffffu, polls);

@@ -22,6 +22,12 @@
 
 namespace qcl {
 
+// Programmatic dependent launch (sm_90+): no-ops when the grid was launched without the
+// programmatic-serialization attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+
 constexpr int kBlock = 256;
 
 struct SlotInfo {      // one rearranged row slot of H_compact1
@@ -447,12 +453,17 @@ __device__ __forceinline__ void check_update(double (&q)[D][V], double (&ph)[D][
 // L is race free.  Offsets inside a lane group are 32-bit (n*W and E*z*W < 2^31).
 template <typename T, int V, int DMAX, bool HAS_SYN>
 __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
-    if (a.n_active && *(volatile const int *)a.n_active == 0) return;
+    // programmatic dependent launch (qcldpc.cu launch_pdl): the next layer's grid may start
+    // now; this one's prologue (immutable plan tables) overlaps the previous layer's tail,
+    // and every read of state the previous kernels wrote follows griddepcontrol.wait
+    pdl_launch_dependents();
     __shared__ EdgeInfo s_edge[DMAX];
     const Item it = map_item<V>(a.r);
     const SlotInfo si = a.r.slots[it.slot];
     const int d = si.degree;
     if (threadIdx.x < d) s_edge[threadIdx.x] = a.r.edges[si.edge_off + threadIdx.x];
+    pdl_wait();
+    if (a.n_active && *(volatile const int *)a.n_active == 0) return;
     __syncthreads();
     if (!it.live) return;
 

@@ -186,6 +186,8 @@ constexpr int pipe_min_blocks() {
 template <typename T, int V, int D, bool HAS_SYN, int C>
 __global__ void __launch_bounds__(32 * (C + 1), (pipe_min_blocks<T, V, D, C>())) layer_tma_kernel(PipeArgs a) {
     constexpr int kConsumerWarps = C;
+    pdl_launch_dependents();  // see layer_kernel
+    pdl_wait();
     if (a.n_active && *(volatile const int *)a.n_active == 0) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw);

@@ -166,12 +166,35 @@ struct qcl_state {
 
 // ----------------------------------------------------------------------------- dispatch
 
+static int env_int(const char *name, int dflt);
+
+// Per-layer kernels are launched with programmatic dependent launch (QCL_PDL, default on):
+// a layer's grid is scheduled while the previous layer drains and waits in
+// griddepcontrol.wait (kernels.cuh) before touching state, which hides most of the
+// launch gap of the ~1500 dependent launches of a per-layer decode (the small-batch and
+// single-codeword path, BASELINE configs[1]).
+template <typename Arg>
+static void launch_pdl(void (*kern)(Arg), dim3 grid, dim3 block, size_t smem, cudaStream_t s, const Arg &a) {
+    static const bool on = env_int("QCL_PDL", 1) != 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = on ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, a);
+}
+
 template <typename T, int V, int DMAX>
 static void launch_layer_t(const LayerArgs &a, dim3 grid, cudaStream_t s, bool syn) {
     if (syn)
-        layer_kernel<T, V, DMAX, true><<<grid, kBlock, 0, s>>>(a);
+        launch_pdl(layer_kernel<T, V, DMAX, true>, grid, dim3(kBlock), 0, s, a);
     else
-        layer_kernel<T, V, DMAX, false><<<grid, kBlock, 0, s>>>(a);
+        launch_pdl(layer_kernel<T, V, DMAX, false>, grid, dim3(kBlock), 0, s, a);
 }
 
 // Only the (V, DMAX) pairs vec_width() can select are instantiated: wide vectors are
@@ -245,7 +268,7 @@ static void launch_tma_tc(const PipeArgs &a, cudaStream_t stream) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, 32 * (C + 1), smem);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
     const int64_t grid = std::min<int64_t>(a.tiles, (int64_t)sms * blocks_per_sm);
-    kern<<<(unsigned)grid, 32 * (C + 1), smem, stream>>>(a);
+    launch_pdl(kern, dim3((unsigned)grid), dim3(32 * (C + 1)), smem, stream, a);
 }
 
 // consumer warps per CTA: 8 by default (QCL_PIPE_WARPS=4 selects the 4-warp variant)
@@ -481,17 +504,18 @@ static int ensure_flow(qcl_state *st, int counters) {
                         for (int kb = 0; kb < nkb[s]; kb++) items.push_back(make_int2(s | (g << 16), kb));
         st->f_sweep_items = (int64_t)items.size() / st->f_nblk;
         CK(cudaMalloc(&st->fslot_tab, sizeof(uint2) * p->S));
-        CK(cudaMemcpy(st->fslot_tab, stab.data(), sizeof(uint2) * p->S, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(st->fslot_tab, stab.data(), sizeof(uint2) * p->S, cudaMemcpyHostToDevice, st->stream));
         CK(cudaMalloc(&st->fitems, sizeof(int2) * items.size()));
-        CK(cudaMemcpy(st->fitems, items.data(), sizeof(int2) * items.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(st->fitems, items.data(), sizeof(int2) * items.size(), cudaMemcpyHostToDevice,
+                           st->stream));
         CK(cudaMalloc(&st->fflags, sizeof(int) * QCL_FLAG_STRIDE * (size_t)st->G * st->f_nkb_total));
         if (env_int("QCL_FLOW_STATS", 0)) {
             CK(cudaMalloc(&st->fstats, 16 * sizeof(unsigned long long)));
-            CK(cudaMemset(st->fstats, 0, 16 * sizeof(unsigned long long)));
+            CK(cudaMemsetAsync(st->fstats, 0, 16 * sizeof(unsigned long long), st->stream));
         }
-        // cudaMemcpy from pageable memory may return before its DMA lands, and the state's
-        // stream does not synchronise with the legacy stream: wait for the uploads here
-        CK(cudaDeviceSynchronize());
+        // the uploads are on the state's stream (a device-wide synchronisation would be
+        // illegal while another host thread captures a decode graph): wait for them here
+        CK(cudaStreamSynchronize(st->stream));
         // ring depth: QCL_FLOW_STAGES (default 3 with two CTAs per SM, 5 with one), reduced
         // until the CTAs fit
         static int want = env_int("QCL_FLOW_STAGES", kFlowCtasPerSm == 1 ? 5 : 3);
@@ -835,23 +859,27 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
     }
     DeviceScope dscope_(device);
     cudaError_t e = dscope_.ok ? cudaSuccess : cudaErrorInvalidDevice;
+    // uploads on a private stream, waited for once (the plan is immutable afterwards and
+    // states run on their own non-blocking streams); no device-wide synchronisation, which
+    // is illegal while another host thread captures a decode graph
+    cudaStream_t up = nullptr;
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking);
+    auto put = [&](void *dst, const void *src, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, up);
+    };
     if (e == cudaSuccess) e = cudaMalloc(&p->fedge_tab, sizeof(uint2) * n_edges);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(p->fedge_tab, h_etab.data(), sizeof(uint2) * n_edges, cudaMemcpyHostToDevice);
+    put(p->fedge_tab, h_etab.data(), sizeof(uint2) * n_edges);
     if (e == cudaSuccess) e = cudaMalloc(&p->slot_list, sizeof(int32_t) * p->h_slot_list.size());
-    if (e == cudaSuccess)
-        e = cudaMemcpy(p->slot_list, p->h_slot_list.data(), sizeof(int32_t) * p->h_slot_list.size(),
-                       cudaMemcpyHostToDevice);
+    put(p->slot_list, p->h_slot_list.data(), sizeof(int32_t) * p->h_slot_list.size());
     if (e == cudaSuccess) e = cudaMalloc(&p->slots, sizeof(SlotInfo) * n_slots);
     if (e == cudaSuccess) e = cudaMalloc(&p->edges, sizeof(EdgeInfo) * n_edges);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(p->slots, p->h_slots.data(), sizeof(SlotInfo) * n_slots, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(p->edges, h_edges.data(), sizeof(EdgeInfo) * n_edges, cudaMemcpyHostToDevice);
-    // the uploads above may still be in flight (pageable-source cudaMemcpy returns once the
-    // data is staged), and states run on non-blocking streams: the plan is immutable after
-    // this point, so wait for it once
-    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    put(p->slots, p->h_slots.data(), sizeof(SlotInfo) * n_slots);
+    put(p->edges, h_edges.data(), sizeof(EdgeInfo) * n_edges);
+    if (up) {
+        const cudaError_t e2 = cudaStreamSynchronize(up);
+        if (e == cudaSuccess) e = e2;
+        cudaStreamDestroy(up);
+    }
     if (e != cudaSuccess) {
         cudaFree(p->slots);
         cudaFree(p->edges);
@@ -915,8 +943,14 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
     st->prec = st->msg16 ? QCL_PREC_FP32 : precision;
     st->esz = st->prec == QCL_PREC_FP32 ? 4 : 8;
     st->resz = st->msg16 ? 2 : st->esz;
-    // FP16 runs of W lanes must stay whole 16-byte bulk-copy units: at least 8 lanes
-    st->lw = st->msg16 ? std::max(3, lanes_log2(batch)) : lanes_log2(batch);
+    // FP16 runs of W lanes must stay whole 16-byte bulk-copy units: at least 8 lanes.
+    // QCL_MIN_LANES=4 pads FP32 batches of 1-3 codewords to 4 lanes (idle lanes decode
+    // zero LLRs) so that they run on the flow engine; off by default: one lane group has
+    // no slack between dependent tiles, and the per-layer graph is faster there (B = 1:
+    // 5.8 ms against 9.1 ms per 50-iteration decode, tools/latency_small_batch.py).
+    static const int min_lanes_f32 = env_int("QCL_MIN_LANES", 1);
+    const int lw_min = st->msg16 ? 3 : st->prec == QCL_PREC_FP32 ? (min_lanes_f32 >= 4 ? 2 : 0) : 0;
+    st->lw = std::max(lw_min, lanes_log2(batch));
     st->W = 1 << st->lw;
     st->G = (int)cdiv(batch, st->W);
     st->Bp = (int64_t)st->G * st->W;

@@ -91,9 +91,32 @@ def test_campaign_two_devices_equal_one(gpu):
 
 
 @pytest.mark.gpu
-def test_campaign_pool_falls_back_when_flow_engine_unsupported(gpu):
-    """Frame pool requested (device channel, ET, FP32) where the flow engine cannot run:
-    2 lanes (batch_size 2) -- the batched device decode runs instead, same outcomes."""
+def test_campaign_pool_falls_back_when_flow_engine_unsupported(gpu, tmp_path):
+    """Frame pool requested (device channel, ET, FP32) on a code the flow engine does not
+    cover (a row of degree 16 > 12): the batched device decode runs instead, with the
+    same per-frame outcomes (it used to raise QCL_EUNSUP)."""
+    import paper_2004_09084_b200 as q
+    from paper_2004_09084_b200.campaign import CampaignConfig, run_campaign
+
+    rng = np.random.default_rng(4)
+    shifts = np.full((3, 20), -1, dtype=np.int64)
+    shifts[0, :16] = rng.integers(0, 16, 16)
+    shifts[1, [0, 3, 16, 17, 18]] = rng.integers(0, 16, 5)
+    shifts[2, [1, 5, 18, 19]] = rng.integers(0, 16, 4)
+    path = tmp_path / "deg16.txt"
+    path.write_text(q.serialize_base_matrix(q.BaseMatrix(3, 20, 16, shifts.tolist())))
+    common = dict(matrix_path=str(path), snr_list=(1.0,), max_iterations=20, early_termination=True,
+                  batch_size=8, min_trials=32, seed=5, channel="device")
+    pooled = run_campaign(CampaignConfig(frame_pool=True, **common))
+    batched = run_campaign(CampaignConfig(frame_pool=False, **common))
+    assert pooled.metadata["device"]["frame_pool"] is False
+    assert [(c.fer, c.avg_iterations) for c in pooled.cells] == [(c.fer, c.avg_iterations) for c in batched.cells]
+
+
+@pytest.mark.gpu
+def test_campaign_pool_with_two_lanes_falls_back(gpu):
+    """batch_size 2 (ADVICE r1's other failing case): two lanes are below the flow
+    engine's 16-byte runs, so the batched decode runs instead, same outcomes."""
     from paper_2004_09084_b200.campaign import CampaignConfig, run_campaign
 
     common = dict(matrix_path=str(CODES / "standin_v2_z100.txt"), snr_list=(0.2,), max_iterations=20,

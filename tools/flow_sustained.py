@@ -53,6 +53,8 @@ th.join()
 half = ms[len(ms) // 2:]
 n = base.n_cols * base.z
 med = statistics.median(half)
-print(f"sustained {a.precision} B={a.batch}: {len(ms)} decodes, median {med:.2f} ms -> {a.batch * n / med / 1e3:.0f} Mbit/s; "
+burst = statistics.median(ms[2:7])
+print(f"sustained {a.precision} B={a.batch}: {len(ms)} decodes, burst (decodes 3-7) {burst:.2f} ms, "
+      f"median {med:.2f} ms -> {a.batch * n / med / 1e3:.0f} Mbit/s; "
       f"sm clock median {statistics.median(c for c, _ in clocks):.0f} MHz, power median "
       f"{statistics.median(p for _, p in clocks):.0f} W", flush=True)

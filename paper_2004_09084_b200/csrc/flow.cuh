@@ -88,9 +88,11 @@ struct FlowArgs {
     const int2 *items;       // per item of one sweep: {slot | g << 16, kb}
     int32_t sweep_items;     // items per sweep of one group block
     uint32_t sweep_mul, sweep_shift;  // x / sweep_items == (umulhi(x, mul) + x) >> shift
-    int32_t blk_items;       // items of this launch per group block (sweeps x sweep_items)
+    int32_t blk_items;       // items of this launch per group block (sweeps x sweep_items [+ tail])
     uint32_t blk_mul, blk_shift;      // x / blk_items, the same way
     int32_t item_end;        // items of this launch (group blocks x blk_items)
+    int32_t tab_stride;      // item-table entries per group block (sweep_items [+ fused-ET tail])
+    int32_t sweeps;          // sweeps of this launch; items past them are the fused-ET tail
     int32_t t_base;          // global sweep index of item 0 (flags count global sweeps)
     const int *t_dev;        // if set: t_base read from device memory (frame-pool sweep graphs)
     int *counter;            // claim counter of this launch (zeroed before it)
@@ -111,6 +113,21 @@ struct FlowArgs {
     unsigned long long *stats;  // optional instrumentation (QCL_FLOW_STATS)
     double clip, eps;
     double mag_max;             // FP32 bound on |r| (LayerArgs::mag_max)
+    // fused early termination (flow_kernel<..., ETF = true>; W <= 8): every sweep of an ET
+    // decode in this one launch, the per-sweep hard decision / syndrome check / freeze as
+    // items of the same stream (see "Fused early termination" below)
+    const uint32_t *slast;   // [S] bit j: edge j of the slot is its column's last writer in a sweep
+    uint8_t *snap;           // [2][G][n] lane bits of the hard decision after sweep t (parity t & 1)
+    uint8_t *fsign;          // [G][n] lane bits frozen at each lane's convergence
+    int *cdone;              // [G] (x QCL_FLAG_STRIDE) check items completed, cumulative
+    int *decided;            // [G] (x QCL_FLAG_STRIDE) sweeps whose ET decision is complete
+    uint32_t *unsat;         // [2][G] (x QCL_FLAG_STRIDE) unsatisfied-lane masks, sweep parity
+    uint32_t *amask;         // [G] lanes still active
+    uint8_t *conv;           // [B] converged flags (decision)
+    int64_t *iters;          // [B] iterations at convergence (decision)
+    const uint32_t *synpack; // [S*z][G] packed target syndrome lane bits (nullptr: all zero)
+    int32_t G;
+    int32_t check_items;     // check items per lane group and sweep (slot ranges)
 };
 
 __host__ __device__ constexpr int flow_class_D(int cls) { return cls == 0 ? 4 : cls == 1 ? 8 : 12; }
@@ -151,8 +168,13 @@ __device__ __forceinline__ int flow_kb_of(int k, int cls, int W, int lw) {
     if constexpr (flow_kt_pow2()) return k >> flow_kt_log2(cls, lw);
     return k / flow_KT(cls, W);
 }
+// shared memory: head (mbarriers, headers) | slot table 8S | edge table 8E | last-writer
+// bits 4S | consumer scratch 16 B | ring stages
+__host__ __device__ constexpr size_t flow_table_end(int S, int E) {
+    return ((kFlowHeadBytes + 8 * (size_t)(S + E) + 4 * (size_t)S + 16 + 127) / 128) * 128;
+}
 __host__ __device__ constexpr size_t flow_smem_bytes(int S, int E, int stages) {
-    return ((kFlowHeadBytes + 8 * (size_t)(S + E) + 127) / 128) * 128 + (size_t)stages * kFlowStageBytes;
+    return flow_table_end(S, E) + (size_t)stages * kFlowStageBytes;
 }
 
 // Item n -> (sweep t relative to t_base, index into the item table), without divisions
@@ -166,7 +188,8 @@ __device__ __forceinline__ int flow_item_map(const FlowArgs &a, int n, int &t) {
     const int b = flow_fastdiv(n, a.blk_mul, a.blk_shift);
     const int r = n - b * a.blk_items;
     t = flow_fastdiv(r, a.sweep_mul, a.sweep_shift);
-    return b * a.sweep_items + (r - t * a.sweep_items);
+    // the fused-ET tail (after the last sweep, t == sweeps) is stored after the sweep table
+    return b * a.tab_stride + (t < a.sweeps ? 0 : a.sweep_items) + (r - t * a.sweep_items);
 }
 inline void flow_sweep_divisor(uint32_t d, uint32_t &mul, uint32_t &shift) {
     uint32_t l = 0;
@@ -231,6 +254,36 @@ __device__ __forceinline__ int spin_until(const int *flag, int need) {
         polls++;
     }
     return polls;
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void spin_until_acquire(const int *flag, int need) {
+    while (ld_acquire_gpu(flag) < need) __nanosleep(128);
+}
+__device__ __forceinline__ void red_release_max(int *p, int v) {
+    asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Tile flag release.  With fused ET a tile of a converged group can be skipped (released at
+// once) while an earlier-sweep tile of the same slot and k-block, resolved before the
+// group converged, is still running: its later release must not lower the flag, or a
+// waiter for the skipped tile's value would wait forever -- hence a max there.
+__device__ __forceinline__ void flag_release(int *p, int v, bool monotonic) {
+    if (monotonic)
+        red_release_max(p, v);
+    else
+        st_release(p, v);
+}
+__device__ __forceinline__ void red_release_add(int *p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int atom_acq_rel_add(int *p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
 }
 
 // Bulk runs of one tile (LOAD: global -> stage, else stage -> global); lane j: edge j.
@@ -339,10 +392,201 @@ __device__ __forceinline__ void consumers_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kFlowConsumers * 32) : "memory");
 }
 
+// ---- Fused early termination ---------------------------------------------------------
+//
+// decode_batch_arrays with early termination (decoder.py:295-305) checks every frame's hard
+// decision against its syndrome after every sweep.  Here that check is part of the flow:
+//  * snapshot: the consumers of a column's LAST writer in sweep t (slast bit) store the lane
+//    bits of the new posteriors' signs as snap[t & 1][g][v] -- the hard decision after
+//    sweep t, taken as it is produced (no pass over L);
+//  * check items (per lane group, one per layer's slot range) of sweep t sit in the item
+//    stream of sweep t + 1, after its first layers -- by then the tiles of sweep t are
+//    stored, so a claimed check rarely waits.  A check item first reads the lanes already
+//    known unsatisfied: if that covers every active lane (nearly always before
+//    convergence) it has nothing to do; otherwise it waits until every tile of (g, t) is
+//    stored (all the group's tile flags >= t + 1), XORs the snapshot bytes of each check
+//    (^ target syndrome), stopping as soon as every active lane is unsatisfied, and ORs
+//    the unsatisfied lanes into unsat[t & 1][g].  The last sweep's checks form a tail
+//    after it;
+//  * the check item that completes (g, t) (cdone) makes the decision: lanes newly satisfied
+//    get converged / iterations = t + 1, their snapshot bits are frozen into fsign, and the
+//    group stops being decoded once all its lanes converged (the rest of the launch skips
+//    its items; once every frame converged the schedulers stop claiming).  Then it
+//    releases decided[g] = t + 1.
+//  * ordering: a tile with last-writer edges at sweep u >= 2 waits decided[g] >= u - 1
+//    (the snapshot parity it overwrites has been read), and the checks of (g, t) wait
+//    decided[g] >= t (decisions of a group stay in sweep order).  All waits point at items
+//    claimed earlier, so the deadlock-freedom argument of the flow kernel holds.
+// Outputs equal the per-sweep check: frames are independent, a converged lane's words are
+// its snapshot at convergence, and lanes still active keep being updated as before.
+
+// number of this warp's consumer lanes whose check lies inside the tile (those that did
+// not return early): the shuffle mask of the snapshot combine
+__device__ __forceinline__ unsigned flow_live_mask(int ct, int lv_log2, int kt) {
+    const int live = (kt << lv_log2) - (ct & ~31);
+    return live >= 32 ? 0xffffffffu : live <= 0 ? 0u : ((1u << live) - 1u);
+}
+
+// Snapshot of one edge's new posteriors x[0..V) (lanes w0..w0+V-1 of check ci): the W/V
+// threads of the check OR their lane bits together; the one holding lane 0 stores the byte.
+template <int V>
+__device__ __forceinline__ void flow_snap(const FlowArgs &a, const FlowHdr &h, uint32_t ex, int ci, int w0,
+                                          const float (&x)[V], unsigned mask) {
+    uint32_t bits = 0;
+#pragma unroll
+    for (int v = 0; v < V; v++) bits |= (uint32_t)(x[v] < 0.0f) << (w0 + v);
+    const int lv = (1 << a.lw) / V;
+    for (int o = 1; o < lv; o <<= 1) bits |= __shfl_xor_sync(mask, bits, o);
+    if (w0 == 0) {
+        const int col = ex & 0x7fff, shift = ex >> 16;
+        int pos = h.k0 + ci + shift;
+        pos -= (pos >= a.z) ? a.z : 0;
+        a.snap[((size_t)(h.t & 1) * a.G + h.g) * a.n + (size_t)col * a.z + pos] = (uint8_t)bits;
+    }
+}
+
+// A check item (g, slots [h.slot, h.kt), sweep h.t), run by all consumer threads of the
+// CTA; sc: 3 words of shared scratch.  See "Fused early termination" above.
+__device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, int ct, const uint2 *stab,
+                                           const uint2 *etab, uint32_t *sc) {
+    constexpr int kThreads = kFlowConsumers * 32;
+    const int g = h.g, t = h.t, par = t & 1, z = a.z;
+    uint32_t *unsat = a.unsat + ((size_t)par * a.G + g) * QCL_FLAG_STRIDE;
+    uint32_t acc = 0;
+    // lanes still to be decided: once every active lane is known unsatisfied (this
+    // sweep's other check items, or this warp's own checks) no further check can change
+    // the decision -- before convergence that is almost immediately, so most check items
+    // scan a few checks, not z per slot
+    const uint32_t need = __ldcg(a.amask + g);
+    const uint32_t known = __ldcg(unsat);
+#ifndef QCL_FLOW_CHECK_EARLY
+#define QCL_FLOW_CHECK_EARLY 1
+#endif
+    const bool scan = need && (!QCL_FLOW_CHECK_EARLY || (known & need) != need) && (!a.gactive || a.gactive[g]);
+    if (scan) {
+        // the snapshot of sweep t is complete once every tile of (g, t) is stored: all tile
+        // flags of the group >= t + 1 (acquire; the barrier passes it to every thread)
+        // relaxed polls, 8 in flight per thread, then one acquire fence per thread
+        const int *fl = a.flags + (size_t)g * a.nkb_total * QCL_FLAG_STRIDE;
+        for (int i0 = ct; i0 < a.nkb_total; i0 += 8 * kThreads) {
+            for (;;) {
+                int v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int i = i0 + u * kThreads;
+                    v[u] = i < a.nkb_total ? ld_flag(fl + (size_t)i * QCL_FLAG_STRIDE) : t + 1;
+                }
+                bool ok = true;
+#pragma unroll
+                for (int u = 0; u < 8; u++) ok &= v[u] >= t + 1;
+                if (ok) break;
+                __nanosleep(128);
+            }
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    consumers_sync();  // uniform: every consumer thread computed the same `scan`
+    if (scan) {
+        const uint8_t *sg = a.snap + ((size_t)par * a.G + g) * a.n;
+        bool done = false;
+        for (int s = h.slot; s < h.kt && !done; s++) {  // h.kt: end of the slot range
+            const uint32_t sx = stab[s].x;
+            const int eo = sx & 0xffff, d = (sx >> 16) & 0xff;
+            // four checks per thread in flight, all d x 4 byte loads (L2 round trips) issued
+            // before the XORs
+            for (int kw = ct & ~31; kw < z; kw += 4 * kThreads) {  // warp-uniform trip count
+                const int k0 = kw + (ct & 31);
+                uint32_t pb[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int k = k0 + u * kThreads;
+                    pb[u] = (a.synpack && k < z) ? __ldg(a.synpack + ((size_t)s * z + k) * a.G + g) : 0u;
+                }
+#pragma unroll
+                for (int j = 0; j < 12; j++) {
+                    if (j < d) {
+                        const uint32_t ex = etab[eo + j].x;
+                        const uint8_t *colp = sg + (size_t)(ex & 0x7fff) * z;
+                        const int sh = (int)(ex >> 16);
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            const int k = k0 + u * kThreads;
+                            int pos = k + sh;
+                            pos -= (pos >= z) ? z : 0;
+                            if (k < z) pb[u] ^= __ldcg(colp + pos);  // L2: written by other CTAs
+                        }
+                    }
+                }
+                acc |= pb[0] | pb[1] | pb[2] | pb[3];
+                if (QCL_FLOW_CHECK_EARLY && ((__reduce_or_sync(0xffffffffu, acc) | known) & need) == need) {
+                    done = true;
+                    break;
+                }
+            }
+        }
+    }
+    acc = __reduce_or_sync(0xffffffffu, acc);
+    if (ct == 0) sc[0] = 0;
+    consumers_sync();
+    if ((ct & 31) == 0 && acc) atomicOr(&sc[0], acc);
+    consumers_sync();
+    if (ct == 0) {
+        if (sc[0]) atomicOr(unsat, sc[0]);
+        __threadfence();
+        const int done = atom_acq_rel_add(a.cdone + (size_t)g * QCL_FLAG_STRIDE, 1) + 1;
+        sc[1] = done == a.check_items * (t + 1);
+    }
+    consumers_sync();
+    if (!sc[1]) return;  // uniform: read after the barrier
+    // ---- decision for (g, t): this item completed the sweep's checks of the group
+    if (ct == 0) {
+        __threadfence();
+        const uint32_t un = *(volatile uint32_t *)unsat;
+        const uint32_t act = a.amask[g];
+        const uint32_t newm = act & ~un;
+        sc[2] = newm;
+        if (newm) {
+            a.amask[g] = act & ~newm;
+            for (uint32_t m = newm; m; m &= m - 1) {
+                const int64_t b = ((int64_t)g << a.lw) + __ffs(m) - 1;
+                a.conv[b] = 1;
+                a.iters[b] = t + 1;
+            }
+            atomicSub(const_cast<int *>(a.n_active), __popc(newm));
+            if (!(act & ~newm)) const_cast<uint8_t *>(a.gactive)[g] = 0;
+        }
+    }
+    consumers_sync();
+    const uint32_t newm = sc[2];
+    if (newm) {  // freeze the newly converged lanes' words: fsign = snap where newm
+        const uint8_t *sg = a.snap + ((size_t)par * a.G + g) * a.n;
+        uint8_t *fg = a.fsign + (size_t)g * a.n;
+        const uint32_t m4 = (newm & 0xffu) * 0x01010101u;
+        const int64_t n16 = (a.n % 16 == 0) ? a.n / 16 : 0;  // 16-byte rows only when n is a multiple
+        for (int64_t i = ct; i < n16; i += kThreads) {
+            const uint4 x = __ldcg(reinterpret_cast<const uint4 *>(sg) + i);
+            uint4 f = reinterpret_cast<uint4 *>(fg)[i];
+            f.x = (f.x & ~m4) | (x.x & m4);
+            f.y = (f.y & ~m4) | (x.y & m4);
+            f.z = (f.z & ~m4) | (x.z & m4);
+            f.w = (f.w & ~m4) | (x.w & m4);
+            reinterpret_cast<uint4 *>(fg)[i] = f;
+        }
+        for (int64_t v = n16 * 16 + ct; v < a.n; v += kThreads)
+            fg[v] = (uint8_t)((fg[v] & ~newm) | (__ldcg(sg + v) & newm));
+    }
+    consumers_sync();
+    if (ct == 0) {
+        *(volatile uint32_t *)unsat = 0;  // reused by sweep t + 2, whose tiles wait for this release
+        __threadfence();
+        st_release(a.decided + (size_t)g * QCL_FLAG_STRIDE, t + 1);
+    }
+}
+
 // One consumer thread: check (ci) of the tile for V lanes, in place in the stage.
-template <int V, int D, bool HAS_SYN, typename RT>
+template <int V, int D, bool HAS_SYN, typename RT, bool ETF>
 __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
-                                             const uint2 *etab) {
+                                             const uint2 *etab, uint32_t lastm) {
     const int W = 1 << a.lw;
     const int KT = flow_kt(h.cls, W, a.lw);
     const int KTW = KT * W;
@@ -399,6 +643,12 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
     } else {
         check_update_f32<V, D, H>(q, ph, par, h.d, (float)a.mag_max, clip);
     }
+    if (ETF && lastm) {  // fused ET: hard-decision snapshot of the columns this slot writes last
+        const unsigned mask = flow_live_mask(ct, lv_log2, h.kt);
+#pragma unroll
+        for (int j = 0; j < D; j++)
+            if (j < h.d && ((lastm >> j) & 1)) flow_snap<V>(a, h, etab[h.edge_off + j].x, ci, w0, q[j], mask);
+    }
 #pragma unroll
     for (int j = 0; j < D; j++) {
         if (j < h.d) {
@@ -419,9 +669,9 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
 // order, as check_update_f32.  With FP16 messages the FP32 stash overlaps other threads'
 // FP16 R values, so all consumers read their inputs before the first stash write and keep
 // the new messages in registers until every thread has read its stash back.
-template <int V, int D, bool HAS_SYN, typename RT>
+template <int V, int D, bool HAS_SYN, typename RT, bool ETF>
 __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
-                                                 const uint2 *etab) {
+                                                 const uint2 *etab, uint32_t lastm) {
     constexpr bool H = sizeof(RT) == 2;
     const int W = 1 << a.lw;
     const int KT = flow_kt(h.cls, W, a.lw);
@@ -499,7 +749,7 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
 #pragma unroll
         for (int j = D - 1; j >= 0; j--) {
             if (j < h.d) {
-                float xs[V], xd[V], rr[V], ll[V];
+                float xs[V], xd[V], rr[V], ll[V], lsn[V];
                 *reinterpret_cast<VT *>(xs) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
                 *reinterpret_cast<VT *>(xd) = *reinterpret_cast<const VT *>(stage + (size_t)(D + j) * KTW + off);
 #pragma unroll
@@ -508,11 +758,14 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
                     const float mag = msg_round<H>(sd_mag(S, Dv, mag_max));
                     rr[v] = ((q[j][v] < 0.0f) ^ (par[v] != 0)) ? -mag : mag;
                     ll[v] = clampT(q[j][v] + rr[v], clip);
+                    lsn[v] = ll[v];  // the new posterior (its sign is the hard decision)
                     if (((dmask >> j) & 1) && !last) ll[v] = clampT(ll[v] - rr[v], clip);  // deferred: next q
                     const float ns = fmaf(t[j][v], sd[v], ss[v]);
                     sd[v] = fmaf(t[j][v], ss[v], sd[v]);
                     ss[v] = ns;
                 }
+                if (ETF && ((lastm >> j) & 1))  // fused ET snapshot of the new posteriors
+                    flow_snap<V>(a, h, etab[h.edge_off + j].x, ci, w0, lsn, flow_live_mask(ct, lv_log2, h.kt));
                 if (H) {  // the R slot may still hold another thread's stash: r waits in q[j]
 #pragma unroll
                     for (int v = 0; v < V; v++) q[j][v] = rr[v];
@@ -540,7 +793,10 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
         tc = c_;                              \
     }
 
-template <bool HAS_SYN, bool PROF, typename RT = float>
+// ETF: fused early termination (a separate instantiation, so that the no-ET kernel carries
+// none of its code: the snapshot path alone cost the no-ET decode ~4% through register
+// allocation)
+template <bool HAS_SYN, bool PROF, typename RT = float, bool ETF = false>
 __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(FlowArgs a) {
     if (a.n_active && *(volatile const int *)a.n_active == 0) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -553,7 +809,9 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
     FlowHdr *hq = hdr + kFlowMaxStages;
     uint2 *stab = reinterpret_cast<uint2 *>(smem_raw + kFlowHeadBytes);
     uint2 *etab = stab + a.S;
-    float *stages = reinterpret_cast<float *>(smem_raw + ((kFlowHeadBytes + 8 * (size_t)(a.S + a.E) + 127) / 128) * 128);
+    uint32_t *slt = reinterpret_cast<uint32_t *>(etab + a.E);  // last-writer bits (fused ET), else 0
+    uint32_t *scratch = slt + a.S;                              // check items (consumers)
+    float *stages = reinterpret_cast<float *>(smem_raw + flow_table_end(a.S, a.E));
     constexpr size_t kStageElems = kFlowStageBytes / 4;
     const int S = a.stages;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -561,6 +819,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
 
     for (int i = threadIdx.x; i < a.S; i += blockDim.x) stab[i] = a.slot_tab[i];
     for (int i = threadIdx.x; i < a.E; i += blockDim.x) etab[i] = a.edge_tab[i];
+    for (int i = threadIdx.x; i < a.S; i += blockDim.x) slt[i] = ETF ? a.slast[i] : 0u;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; s++) {
             mbar_init(&full[s], 1);
@@ -586,9 +845,12 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         const int t_base = a.t_dev ? *(volatile const int *)a.t_dev : a.t_base;
         int n2 = 0;
         if (lane == 0) n2 = atomicAdd(a.counter, 1);
+        // stop: every frame converged (fused ET) -- the items already claimed (the one in
+        // hand and the prefetched one) are still processed, nothing new is claimed
+        bool stop = false;
         auto next_claim = [&]() {
             const int n = __shfl_sync(0xffffffffu, n2, 0);
-            if (n < a.item_end && lane == 0) n2 = atomicAdd(a.counter, 1);
+            if (n < a.item_end && lane == 0) n2 = stop ? a.item_end : atomicAdd(a.counter, 1);
             return n;
         };
         auto record = [&](int n) {
@@ -600,6 +862,10 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         if (n1 < a.item_end) r1 = record(n1);
         int sentinels = 0;
         unsigned long long n_waited = 0, n_polls = 0, n_tiles = 0;
+        // fused ET: lane (g & 31) caches the largest decided[g] it has observed (monotonic),
+        // so the snapshot-reuse gate costs an L2 round trip once per group and sweep, not
+        // once per tile
+        int dec_tag = -1, dec_val = 0;
         // lane j < d: the flags of the previous writer of edge j's column covering this
         // tile's offsets (kb in [lo, lo + nlo) and, past the wrap at z, [0, nfl - nlo))
         auto flag_plan = [&](const FlowHdr &h, const int *&fl, int &need, int &lo, int &nlo, int &nfl) {
@@ -629,6 +895,12 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             h.edge_off = st.x & 0xffff;
             h.d = (st.x >> 16) & 0xff;
             h.cls = st.x >> 24;
+            if (e.y < 0) {  // fused-ET check item: every check of slots [slot, -1 - e.y) after the
+                h.k0 = -1;  // PREVIOUS sweep (the items of sweep t's checks sit in sweep t + 1's
+                h.kt = -1 - e.y;  // stream, so their tiles are long stored when they are claimed)
+                h.t -= 1;
+                return h;
+            }
             const int KT = flow_kt(h.cls, W, a.lw);
             h.k0 = e.y * KT;
             h.kt = min(KT, a.z - h.k0);
@@ -652,17 +924,46 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 if (n1 < a.item_end) r1 = record(n1);
                 FLOW_TICK(1);
                 const FlowHdr h = resolve(item, e);
-                if (a.gactive && !a.gactive[h.g]) {
+                if (h.k0 < 0 && h.t < 0) {  // the first sweep's check items (of sweep -1): nothing
+                    __syncwarp();
+                    goto next_item;
+                }
+                if (h.k0 >= 0 && a.gactive && !a.gactive[h.g]) {
                     // every frame of this lane group has converged: its outputs are frozen,
                     // so the tile is not updated -- only released for the group's later tiles
                     __syncwarp();
-                    if (lane == 0) st_release(a.flags + ((size_t)h.g * a.nkb_total + stab[h.slot].y + e.y) * QCL_FLAG_STRIDE, h.t + 1);
+                    if (lane == 0) {
+                        flag_release(a.flags + ((size_t)h.g * a.nkb_total + stab[h.slot].y + e.y) * QCL_FLAG_STRIDE, h.t + 1,
+                                     ETF);
+                    }
+#ifndef QCL_FLOW_ET_STOP
+#define QCL_FLOW_ET_STOP 1
+#endif
+                    if (QCL_FLOW_ET_STOP && ETF) {
+                        int none = 0;
+                        if (lane == 0) none = *(volatile const int *)a.n_active == 0;
+                        stop = stop || __shfl_sync(0xffffffffu, none, 0);
+                    }
                     goto next_item;
                 }
                 // wait for the previous writers of every column of this tile: all covering
                 // flags of an edge are loaded together (one round trip), only stale ones polled
                 int polls = 0;
-                {
+                if (h.k0 < 0) {
+                    // check item (g, slot, t): every tile of (g, t) stored, decisions in order
+                    if (lane == 0 && h.t >= 1) spin_until_acquire(a.decided + (size_t)h.g * QCL_FLAG_STRIDE, h.t);
+                    __syncwarp();
+                } else {
+                    if (ETF && slt[h.slot] && h.t >= 2) {  // snapshot parity reuse
+                        const int owner = h.g & 31;
+                        const bool cached = __shfl_sync(0xffffffffu, dec_tag == h.g && dec_val >= h.t - 1, owner);
+                        if (!cached && lane == owner) {
+                            const int *dp = a.decided + (size_t)h.g * QCL_FLAG_STRIDE;
+                            polls += spin_until(dp, h.t - 1);
+                            dec_tag = h.g;
+                            dec_val = h.t - 1;
+                        }
+                    }
                     const int *fl = nullptr;
                     int need = 0, lo = 0, nlo = 0, nfl = 0, fv[4];
                     flag_plan(h, fl, need, lo, nlo, nfl);
@@ -731,6 +1032,12 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                     mbar_arrive(&full[s]);
                 }
                 if (++sentinels == kFlowStorers) break;
+            } else if (h.k0 < 0) {  // fused-ET check item: no bulk data, the consumers read L2
+                if (lane == 0) {
+                    hdr[s] = h;
+                    mbar_arrive(&full[s]);
+                }
+                __syncwarp();
             } else {
                 fence_proxy_async_global();  // observed flags -> ordered before the bulk (async proxy) reads
                 const int KT = flow_kt(h.cls, W, a.lw);
@@ -773,6 +1080,11 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             if (sprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
             const FlowHdr h = hdr[s];
             if (h.kt < 0) break;
+            if (h.k0 < 0) {  // check item: nothing to store
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+                continue;
+            }
             const int KT = flow_kt(h.cls, W, a.lw);
             flow_runs<RT>(a, h, etab, KT, flow_class_D(h.cls), stages + (size_t)s * kStageElems, nullptr, false,
                       pol_keep, pol_stream);
@@ -786,8 +1098,8 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             fence_proxy_async_global();
             __syncwarp();
             if (lane == 0) {  // ... before the tile is released to its dependents
-                st_release(a.flags + ((size_t)h.g * a.nkb_total + stab[h.slot].y + flow_kb_of(h.k0, h.cls, W, a.lw)) * QCL_FLAG_STRIDE,
-                           h.t + 1);
+                flag_release(a.flags + ((size_t)h.g * a.nkb_total + stab[h.slot].y + flow_kb_of(h.k0, h.cls, W, a.lw)) * QCL_FLAG_STRIDE,
+                             h.t + 1, ETF);
             }
             if (sprof) acc[3] += clock64() - tc;
         }
@@ -810,12 +1122,15 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             if (++sentinels == kFlowStorers) break;
         } else {
             float *stage = stages + (size_t)s * kStageElems;
-            if (h.cls == 0)
-                flow_consume<flow_class_V(0), 4, HAS_SYN, RT>(a, h, stage, ct, etab);
-            else if (h.cls == 1)
-                flow_consume_gen<flow_class_V(1), 8, HAS_SYN, RT>(a, h, stage, ct, etab);
-            else
-                flow_consume_gen<flow_class_V(2), 12, HAS_SYN, RT>(a, h, stage, ct, etab);
+            if (ETF && h.k0 < 0) {
+                if constexpr (ETF) flow_check(a, h, ct, stab, etab, scratch);
+            } else if (h.cls == 0) {
+                flow_consume<flow_class_V(0), 4, HAS_SYN, RT, ETF>(a, h, stage, ct, etab, slt[h.slot]);
+            } else if (h.cls == 1) {
+                flow_consume_gen<flow_class_V(1), 8, HAS_SYN, RT, ETF>(a, h, stage, ct, etab, slt[h.slot]);
+            } else {
+                flow_consume_gen<flow_class_V(2), 12, HAS_SYN, RT, ETF>(a, h, stage, ct, etab, slt[h.slot]);
+            }
             fence_proxy_async_smem();  // this thread's STS -> visible to the bulk-store engine
             __syncwarp();
             if (lane == 0) mbar_arrive(&done[s]);

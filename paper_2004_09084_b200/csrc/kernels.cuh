@@ -678,6 +678,44 @@ __global__ void __launch_bounds__(kBlock) words_from_signs_kernel(const uint32_t
     }
 }
 
+// Fused early termination (flow.cuh): active-lane masks at the start of a decode, and the
+// words afterwards -- a converged codeword's lane bits frozen at its convergence (fsign),
+// any other's from the hard-decision snapshot of the last sweep (decoder.py:307-311).
+__global__ void amask_init_kernel(int G, int lw, int64_t B, uint32_t *amask) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    const int64_t live = B - ((int64_t)g << lw);
+    const int W = 1 << lw;
+    amask[g] = live >= W ? (W == 32 ? 0xffffffffu : (1u << W) - 1u) : live <= 0 ? 0u : (1u << live) - 1u;
+}
+
+// Snapshot lane bits (both sweep parities) of the variables of columns no row touches.
+__global__ void snap_untouched_kernel(const float *L, const int32_t *cols, int ncols, int z, int64_t n, int G,
+                                      int lw, uint8_t *snap) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t per_g = (int64_t)ncols * z;
+    if (i >= per_g * G) return;
+    const int64_t g = i / per_g, r = i - g * per_g;
+    const int64_t v = (int64_t)cols[r / z] * z + r % z;
+    const int W = 1 << lw;
+    uint32_t bits = 0;
+    for (int w = 0; w < W; w++) bits |= (uint32_t)(L[((g * n + v) << lw) + w] < 0.0f) << w;
+    snap[g * n + v] = (uint8_t)bits;
+    snap[((int64_t)G + g) * n + v] = (uint8_t)bits;
+}
+
+__global__ void __launch_bounds__(kBlock) et_words_kernel(const uint8_t *snap_last, const uint8_t *fsign,
+                                                          const uint8_t *conv, int64_t n, int lw, int64_t B,
+                                                          uint8_t *words) {
+    const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const int Wm = (1 << lw) - 1;
+    for (int64_t b = 0; b < B; b++) {
+        const uint8_t *src = conv[b] ? fsign : snap_last;
+        words[b * n + v] = (uint8_t)((src[(b >> lw) * n + v] >> (b & Wm)) & 1u);
+    }
+}
+
 __device__ __forceinline__ uint8_t lane_unsat(const uint32_t *mask, int64_t b, int lw) {
     return (uint8_t)((mask[b >> lw] >> (b & ((1 << lw) - 1))) & 1u);
 }

@@ -92,6 +92,9 @@ struct qcl_plan {
     SlotInfo *slots = nullptr;  // device H_compact1: per slot
     EdgeInfo *edges = nullptr;  // device H_compact1: per circulant
     uint2 *fedge_tab = nullptr;  // device, flow engine: packed circulant + previous-writer table
+    uint32_t *fslast = nullptr;  // device, flow engine: per slot, bit j = edge j writes its column last
+    int32_t *funtouched = nullptr;  // device: columns no row touches (their decisions never change)
+    int n_untouched = 0;
     bool flow_ok = false;        // the code fits the flow engine's packed tables
     std::vector<int32_t> h_edge_shift, h_edge_col;
     std::mutex cache_mu;
@@ -152,6 +155,15 @@ struct qcl_state {
     int32_t f_nblk = 1;         // group blocks (flow.cuh flow_item_map)
     int32_t f_nkb_total = 0, f_counter_cap = 0, f_grid = 0, f_stages = 3;
     bool flow_decode = false;  // this decode runs on the flow engine
+    bool fused_et = false;     // this decode's early termination runs inside the flow launch
+    // fused early termination (flow.cuh): item list with check items, snapshot buffers
+    int2 *fitems_et = nullptr;
+    int64_t f_sweep_items_et = 0;  // per sweep of one group block (its table adds a tail)
+    int32_t f_check_items = 0;     // check items per lane group and sweep
+    uint8_t *fsnap = nullptr;   // [2][G][n]
+    uint8_t *fsign = nullptr;   // [G][n]
+    int *fet = nullptr;         // cdone | decided | unsat[2], each [G] x QCL_FLAG_STRIDE
+    uint32_t *famask = nullptr; // [G]
     // frame pool (qcl_state_decode_pool): per lane frame index / iterations, refill list
     bool pool_active = false;
     int64_t *pframe = nullptr;     // [Bp] frame decoded by the lane, -1 idle
@@ -533,7 +545,9 @@ static int ensure_flow(qcl_state *st, int counters) {
         st->f_stages = stages;
         for (auto kern : {flow_kernel<false, false>, flow_kernel<true, false>, flow_kernel<false, true>,
                           flow_kernel<true, true>, flow_kernel<false, false, __half>, flow_kernel<true, false, __half>,
-                          flow_kernel<false, true, __half>, flow_kernel<true, true, __half>})
+                          flow_kernel<false, true, __half>, flow_kernel<true, true, __half>,
+                          flow_kernel<false, false, float, true>, flow_kernel<true, false, float, true>,
+                          flow_kernel<false, false, __half, true>, flow_kernel<true, false, __half, true>})
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, flow_kernel<false, false>, kFlowThreads, smem));
         st->f_grid = sms * std::max(1, per_sm);
@@ -545,6 +559,55 @@ static int ensure_flow(qcl_state *st, int counters) {
         CK(cudaMalloc(&st->fcounters, sizeof(int) * counters));
         st->f_counter_cap = counters;
     }
+    return QCL_OK;
+}
+
+// Fused early termination (flow.cuh): ET decodes on the flow engine run every sweep in one
+// launch, with the per-sweep check as items of the same stream.  Needs W <= 8 (one byte of
+// lane bits per variable); the frame pool keeps its per-sweep launches (lanes refill).
+// QCL_FLOW_ET_FUSED=0: the per-sweep launch plus check kernels of round 1.
+static bool use_flow_et(const qcl_state *st) {
+    static const bool on = env_int("QCL_FLOW_ET_FUSED", 1) != 0;
+    return on && use_flow(st) && st->W <= 8 && !st->pool_active;
+}
+
+static int ensure_flow_et(qcl_state *st) {
+    const qcl_plan *p = st->plan;
+    if (st->fitems_et) return QCL_OK;
+    static const int blk_groups = env_int("QCL_FLOW_BLOCK_GROUPS", 8);
+    const int GB = st->G / st->f_nblk;
+    (void)blk_groups;
+    // per group block: the sweep table -- layers 0..Lc, the check items of the PREVIOUS sweep
+    // (one per lane group and layer: slots [s0, s1) as {s0 | g << 16, -1 - s1}), the other
+    // layers -- then a tail with the last sweep's check items (flow.cuh flow_item_map)
+    const int Lc = std::min(1, p->n_layers - 1);
+    std::vector<int2> items, checks;
+    for (int b = 0; b < st->f_nblk; b++) {
+        checks.clear();
+        for (int g = b * GB; g < (b + 1) * GB; g++)
+            for (int l = 0; l < p->n_layers; l++)
+                checks.push_back(make_int2(p->layer_start[l] | (g << 16), -1 - p->layer_start[l + 1]));
+        for (int l = 0; l < p->n_layers; l++) {
+            for (int g = b * GB; g < (b + 1) * GB; g++)
+                for (int s = p->layer_start[l]; s < p->layer_start[l + 1]; s++) {
+                    const int d = p->h_slots[s].degree;
+                    const int KT = flow_KT(d <= 4 ? 0 : d <= 8 ? 1 : 2, st->W);
+                    for (int kb = 0; kb < (int)cdiv(p->z, KT); kb++) items.push_back(make_int2(s | (g << 16), kb));
+                }
+            if (l == Lc) items.insert(items.end(), checks.begin(), checks.end());
+        }
+        items.insert(items.end(), checks.begin(), checks.end());  // tail
+    }
+    st->f_check_items = p->n_layers;
+    st->f_sweep_items_et = (int64_t)items.size() / st->f_nblk - (int64_t)GB * p->n_layers;
+    CK(cudaMalloc(&st->fitems_et, sizeof(int2) * items.size()));
+    CK(cudaMemcpyAsync(st->fitems_et, items.data(), sizeof(int2) * items.size(), cudaMemcpyHostToDevice,
+                       st->stream));
+    CK(cudaMalloc(&st->fsnap, (size_t)2 * st->G * p->n));
+    CK(cudaMalloc(&st->fsign, (size_t)st->G * p->n));
+    CK(cudaMalloc(&st->fet, sizeof(int) * 4 * QCL_FLAG_STRIDE * (size_t)st->G));
+    CK(cudaMalloc(&st->famask, sizeof(uint32_t) * st->G));
+    CK(cudaStreamSynchronize(st->stream));
     return QCL_OK;
 }
 
@@ -565,17 +628,36 @@ static int enqueue_flow_reset(qcl_state *st, int counters) {
 
 // Sweeps [t0, t0 + T) in one persistent launch using claim counter `counter`.
 static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, int counter, bool et,
-                        int defer_last = -1, const int *t_dev = nullptr, int fresh_t = -1) {
+                        int defer_last = -1, const int *t_dev = nullptr, int fresh_t = -1, bool etf = false) {
     const qcl_plan *p = st->plan;
-    FlowArgs a;
+    FlowArgs a = {};
+    const int64_t sweep_items = etf ? st->f_sweep_items_et : st->f_sweep_items;
     a.slot_tab = st->fslot_tab;
     a.edge_tab = p->fedge_tab;
-    a.items = st->fitems;
-    a.sweep_items = (int32_t)st->f_sweep_items;
-    flow_sweep_divisor((uint32_t)st->f_sweep_items, a.sweep_mul, a.sweep_shift);
-    a.blk_items = (int32_t)(T * st->f_sweep_items);
+    a.items = etf ? st->fitems_et : st->fitems;
+    a.sweep_items = (int32_t)sweep_items;
+    flow_sweep_divisor((uint32_t)sweep_items, a.sweep_mul, a.sweep_shift);
+    const int64_t tail = etf ? (int64_t)(st->G / st->f_nblk) * st->f_check_items : 0;
+    a.blk_items = (int32_t)(T * sweep_items + tail);
     flow_sweep_divisor((uint32_t)a.blk_items, a.blk_mul, a.blk_shift);
-    a.item_end = (int32_t)(st->f_nblk * T * st->f_sweep_items);
+    a.item_end = (int32_t)(st->f_nblk * a.blk_items);
+    a.tab_stride = (int32_t)(sweep_items + tail);
+    a.sweeps = T;
+    a.check_items = st->f_check_items;
+    if (etf) {
+        const size_t gs = (size_t)st->G * QCL_FLAG_STRIDE;
+        a.slast = p->fslast;
+        a.snap = st->fsnap;
+        a.fsign = st->fsign;
+        a.cdone = st->fet;
+        a.decided = st->fet + gs;
+        a.unsat = reinterpret_cast<uint32_t *>(st->fet + 2 * gs);
+        a.amask = st->famask;
+        a.conv = st->conv;
+        a.iters = st->iters;
+        a.synpack = st->has_syn ? st->synpack : nullptr;
+    }
+    a.G = st->G;
     a.t_base = t0;
     a.t_dev = t_dev;
     a.fresh_t = fresh_t;
@@ -604,7 +686,10 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     const int64_t grid = std::min<int64_t>(st->f_grid, a.item_end);
     const bool prof = st->fstats != nullptr;
     void (*kern)(FlowArgs);
-    if (st->msg16)
+    if (etf)  // fused early termination (no instrumented variant)
+        kern = st->msg16 ? (st->has_syn ? flow_kernel<true, false, __half, true> : flow_kernel<false, false, __half, true>)
+                         : (st->has_syn ? flow_kernel<true, false, float, true> : flow_kernel<false, false, float, true>);
+    else if (st->msg16)
         kern = st->has_syn ? (prof ? flow_kernel<true, true, __half> : flow_kernel<true, false, __half>)
                            : (prof ? flow_kernel<false, true, __half> : flow_kernel<false, false, __half>);
     else
@@ -838,6 +923,7 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
     // (= slot) order; the first toucher of a column waits on the last one of the previous
     // iteration (itself for a degree-1 column).  Packed as in csrc/flow.cuh.
     std::vector<uint2> h_etab(n_edges);
+    std::vector<uint32_t> h_slast(n_slots, 0u);
     p->flow_ok = z <= 65535 && n_cols <= 32767 && n_slots <= 32767 && n_edges <= 65535;
     {
         std::vector<std::vector<int>> touch(n_cols);  // circulants per column, slot order
@@ -854,6 +940,8 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
                 const uint32_t reused = tl.size() > 1;
                 h_etab[e].x = (uint32_t)(c & 0x7fff) | (reused << 15) | ((uint32_t)edge_shift[e] << 16);
                 h_etab[e].y = (uint32_t)(slot_of[pe] & 0x7fff) | ((i == 0 ? 1u : 0u) << 15) | ((uint32_t)delta << 16);
+                if (i + 1 == tl.size() && e - slot_offsets[slot_of[e]] < 32)
+                    h_slast[slot_of[e]] |= 1u << (e - slot_offsets[slot_of[e]]);
             }
         }
     }
@@ -869,6 +957,18 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
     };
     if (e == cudaSuccess) e = cudaMalloc(&p->fedge_tab, sizeof(uint2) * n_edges);
     put(p->fedge_tab, h_etab.data(), sizeof(uint2) * n_edges);
+    if (e == cudaSuccess) e = cudaMalloc(&p->fslast, sizeof(uint32_t) * n_slots);
+    put(p->fslast, h_slast.data(), sizeof(uint32_t) * n_slots);
+    std::vector<int32_t> untouched;
+    {
+        std::vector<char> used(n_cols, 0);
+        for (int i = 0; i < n_edges; i++) used[edge_col[i]] = 1;
+        for (int c = 0; c < n_cols; c++)
+            if (!used[c]) untouched.push_back(c);
+    }
+    p->n_untouched = (int)untouched.size();
+    if (e == cudaSuccess && !untouched.empty()) e = cudaMalloc(&p->funtouched, sizeof(int32_t) * untouched.size());
+    if (!untouched.empty()) put(p->funtouched, untouched.data(), sizeof(int32_t) * untouched.size());
     if (e == cudaSuccess) e = cudaMalloc(&p->slot_list, sizeof(int32_t) * p->h_slot_list.size());
     put(p->slot_list, p->h_slot_list.data(), sizeof(int32_t) * p->h_slot_list.size());
     if (e == cudaSuccess) e = cudaMalloc(&p->slots, sizeof(SlotInfo) * n_slots);
@@ -885,6 +985,8 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
         cudaFree(p->edges);
         cudaFree(p->slot_list);
         cudaFree(p->fedge_tab);
+        cudaFree(p->fslast);
+        cudaFree(p->funtouched);
         delete p;
         return fail(QCL_ECUDA, "plan upload failed: %s", cudaGetErrorString(e));
     }
@@ -902,6 +1004,8 @@ int qcl_plan_destroy(qcl_plan *p) {
     cudaFree(p->edges);
     cudaFree(p->slot_list);
     cudaFree(p->fedge_tab);
+    cudaFree(p->fslast);
+    cudaFree(p->funtouched);
     delete p;
     return QCL_OK;
 }
@@ -1022,7 +1126,9 @@ int qcl_state_destroy(qcl_state *st) {
                       (void *)st->n_active, (void *)st->truths, st->staging, (void *)st->fslot_tab,
                       (void *)st->pframe, (void *)st->piter, (void *)st->pfresh, (void *)st->plane_any,
                       (void *)st->prefill, (void *)st->pcount,
-                      (void *)st->fitems, (void *)st->fflags, (void *)st->fcounters, (void *)st->fstats})
+                      (void *)st->fitems, (void *)st->fflags, (void *)st->fcounters, (void *)st->fstats,
+                      (void *)st->fitems_et, (void *)st->fsnap, (void *)st->fsign, (void *)st->fet,
+                      (void *)st->famask})
         if (ptr) cudaFree(ptr);
     if (st->h_n_active) cudaFreeHost(st->h_n_active);
     if (st->h_flag) cudaFreeHost(st->h_flag);
@@ -1388,10 +1494,56 @@ static int validate_cfg(const qcl_config *cfg) {
 // The decode body without host synchronisation: init, reset, the sweeps (and per-sweep
 // early-termination bookkeeping), final check and words.  Captured once into a
 // whole-decode graph; the only host work per decode is then one graph launch.
+// Early-termination decode on the flow engine with the per-sweep check fused into the one
+// launch (flow.cuh, "Fused early termination"): init, reset, flags/counters, the launch
+// (CUDA events around it when profiling), words.
+static int enqueue_decode_fused_et(qcl_state *st, const qcl_config *cfg) {
+    int rc;
+    const qcl_plan *p = st->plan;
+    decode_init_kernel<<<(unsigned)cdiv(st->Bp, kBlock), kBlock, 0, st->stream>>>(
+        st->B, st->Bp, cfg->max_iterations, st->active, st->conv, st->iters, st->n_active);
+    enqueue_group_active(st);
+    amask_init_kernel<<<(unsigned)cdiv(st->G, kBlock), kBlock, 0, st->stream>>>(st->G, st->lw, st->B, st->famask);
+    st->launches_all += 2;
+    st->g_et = true;
+    if ((rc = enqueue_reset(st, cfg->llr_clip, false))) return rc;  // sweep 0 zeroes r_old itself
+    if (p->n_untouched) {  // columns without edges: no tile writes their snapshot; L never changes
+        const int64_t total = (int64_t)st->G * p->n_untouched * p->z;
+        snap_untouched_kernel<<<(unsigned)cdiv(total, kBlock), kBlock, 0, st->stream>>>(
+            (const float *)st->L, p->funtouched, p->n_untouched, p->z, p->n, st->G, st->lw, st->fsnap);
+        st->launches_all++;
+    }
+    if ((rc = enqueue_flow_reset(st, 1))) return rc;
+    CK(cudaMemsetAsync(st->fet, 0, sizeof(int) * 4 * QCL_FLAG_STRIDE * (size_t)st->G, st->stream));
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (st->profiling) {
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        CK(cudaEventRecord(a, st->stream));
+    }
+    // degree-1 deferral as in the no-ET decode: the snapshots take the true posteriors; a
+    // decode that stops early leaves the degree-1 columns' L slots holding the next sweep's
+    // q (only qcl_state_download sees that; words, flags and iterations do not)
+    if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, 0, cfg->max_iterations, 0, true,
+                           flow_defer_last(cfg->max_iterations), nullptr, 0, true)))
+        return rc;
+    if (st->profiling) {
+        CK(cudaEventRecord(b, st->stream));
+        st->sweep_events.push_back({a, b});
+    }
+    const uint8_t *snap_last = st->fsnap + (size_t)((cfg->max_iterations - 1) & 1) * st->G * p->n;
+    et_words_kernel<<<(unsigned)cdiv(p->n, kBlock), kBlock, 0, st->stream>>>(snap_last, st->fsign, st->conv, p->n,
+                                                                              st->lw, st->B, st->words);
+    st->launches_all++;
+    CK(cudaGetLastError());
+    return QCL_OK;
+}
+
 static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
     int rc;
     const unsigned gb = (unsigned)cdiv(st->B, kBlock);
     const bool et = cfg->early_termination != 0;
+    if (et && st->fused_et) return enqueue_decode_fused_et(st, cfg);
     decode_init_kernel<<<(unsigned)cdiv(st->Bp, kBlock), kBlock, 0, st->stream>>>(
         st->B, st->Bp, cfg->max_iterations, st->active, st->conv, st->iters, st->n_active);
     st->launches_all++;
@@ -1453,7 +1605,19 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
     st->flow_decode = use_flow(st) && (int64_t)cfg->max_iterations * st->f_sweep_items * st->f_nblk + 8LL * st->f_grid <
                                            (1LL << 31);
     if (st->msg16 && !st->flow_decode) return msg16_unsupported(st, "this decode");
-    if (!st->profiling && !(sync && et)) {
+    bool fused = false;
+    if (et && st->flow_decode && use_flow_et(st)) {
+        if ((rc = ensure_flow_et(st))) return rc;
+        fused = (int64_t)cfg->max_iterations * st->f_sweep_items_et * st->f_nblk + 8LL * st->f_grid < (1LL << 31);
+    }
+    st->fused_et = fused;
+    if (fused && st->profiling) {
+        CK(cudaEventRecord(st->ev0, st->stream));
+        if ((rc = enqueue_decode_fused_et(st, cfg))) return rc;
+        CK(cudaEventRecord(st->ev1, st->stream));
+        return QCL_OK;
+    }
+    if (!st->profiling && !(sync && et && !fused)) {
         const bool stale = !st->decode_exec || st->d_clip != cfg->llr_clip || st->d_eps != cfg->phi_epsilon ||
                            st->d_syn != st->has_syn || st->d_et != et || st->d_iters != cfg->max_iterations ||
                            st->d_engine != st->engine;

@@ -82,6 +82,32 @@ def test_flow_early_termination_matches(gpu, snr):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("batch,snr", [(64, 0.18), (128, 0.2), (21, 0.19)])
+def test_fused_early_termination_repeated(gpu, batch, snr):
+    """ET inside the flow launch (flow.cuh, "Fused early termination"): random codewords
+    with their nonzero targets (encode mode), one and two group blocks, a ragged lane group; repeated decodes (every run
+    interleaves tiles, checks and decisions differently) equal the per-layer engine's
+    per-sweep check: words, converged flags, iteration counts."""
+    from paper_2004_09084_b200 import _native
+    import paper_2004_09084_b200 as q
+
+    base, sched, index = load_code("standin_v2_z100")
+    plan = _native.Plan(index, sched, 0)
+    cfg = _native.make_config(q.DecoderConfig(max_iterations=40, early_termination=True), "fp32")
+    outs = []
+    for engine in (0, 4, 4, 4):
+        st = _native.State(plan, batch, "fp32")
+        st.set_engine(engine)
+        st.set_llr_synthetic(seed=5, snr_idx=1, first_frame=0, snr=snr, encode_mode=True)  # random words, H c
+        st.decode(cfg)
+        outs.append(st.results())
+    want = outs[0]
+    assert want[1].any()  # some frames converge, some (possibly) do not
+    for got in outs[1:]:
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
+
+
 def test_flow_fresh_states_first_launch(gpu):
     """A new decoder's first decode (table uploads immediately followed by the launch)."""
     import paper_2004_09084_b200 as q

@@ -89,6 +89,8 @@ def lib():
             )
         handle = ctypes.CDLL(str(LIB_PATH))
         for name, (args, res) in _SIGNATURES.items():
+            if os.environ.get("QCL_LIB_VARIANT") and not hasattr(handle, name):
+                continue  # an older build under A/B (tools/): symbols it predates are absent
             fn = getattr(handle, name)
             fn.argtypes = args
             fn.restype = res

@@ -104,6 +104,8 @@ struct FlowArgs {
     int32_t E, S, z, lw;
     int32_t stages;
     int32_t clip_r;
+    const uint32_t *slot_mask;  // [S] bits 0-15: edge j's column is degree 1 (deferrable);
+                                // bits 16-31: edge j is its column's last writer in a sweep
     const int *n_active;  // early termination: skip the launch once every frame converged
     const uint8_t *gactive;  // early termination: lane groups with an active frame (others skipped)
     int32_t defer_last;      // >= 0: degree-1 edges keep q in the L slot and no R until sweep defer_last
@@ -113,10 +115,11 @@ struct FlowArgs {
     unsigned long long *stats;  // optional instrumentation (QCL_FLOW_STATS)
     double clip, eps;
     double mag_max;             // FP32 bound on |r| (LayerArgs::mag_max)
+    float clip_f, mag_f;        // the same two, rounded to FP32 once on the host
     // fused early termination (flow_kernel<..., ETF = true>; W <= 8): every sweep of an ET
     // decode in this one launch, the per-sweep hard decision / syndrome check / freeze as
     // items of the same stream (see "Fused early termination" below)
-    const uint32_t *slast;   // [S] bit j: edge j of the slot is its column's last writer in a sweep
+
     uint8_t *snap;           // [2][G][n] lane bits of the hard decision after sweep t (parity t & 1)
     uint8_t *fsign;          // [G][n] lane bits frozen at each lane's convergence
     int *cdone;              // [G] (x QCL_FLAG_STRIDE) check items completed, cumulative
@@ -338,11 +341,8 @@ __device__ __forceinline__ void flow_runs(const FlowArgs &a, const FlowHdr &h, c
 // last sweep (t == defer_last) writes the true L = clip(q + r) and R = r, so the final
 // state equals the undeferred one bit for bit.  Saves 8 of the 16 bytes per degree-1 edge
 // and sweep (23% of the edges of the rate-0.1 code, ~19% of its DRAM traffic).
-__device__ __forceinline__ uint32_t flow_deferred_mask(const FlowArgs &a, const FlowHdr &h, const uint2 *etab) {
-    if (a.defer_last < 0) return 0u;
-    uint32_t m = 0;
-    for (int j = 0; j < h.d; j++) m |= (((etab[h.edge_off + j].x >> 15) & 1u) ^ 1u) << j;
-    return m;
+__device__ __forceinline__ uint32_t flow_deferred_mask(const FlowArgs &a, uint32_t smask) {
+    return a.defer_last >= 0 ? (smask & 0xffffu) : 0u;  // bit j: edge j's column is degree 1
 }
 
 // V consecutive edge messages of one check <-> registers (FP32 or FP16 in the stage).
@@ -586,7 +586,8 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
 // One consumer thread: check (ci) of the tile for V lanes, in place in the stage.
 template <int V, int D, bool HAS_SYN, typename RT, bool ETF>
 __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
-                                             const uint2 *etab, uint32_t lastm) {
+                                             const uint2 *etab, uint32_t smask) {
+    const uint32_t lastm = smask >> 16;
     const int W = 1 << a.lw;
     const int KT = flow_kt(h.cls, W, a.lw);
     const int KTW = KT * W;
@@ -595,12 +596,12 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
     const int w0 = (ct - (ci << lv_log2)) * V;
     if (ci >= h.kt) return;
     const int off = ci * W + w0;
-    const float clip = (float)a.clip;
+    const float clip = a.clip_f;
     constexpr bool H = sizeof(RT) == 2;
     using VT = typename Vec<float, V>::type;
     float q[D][V], ph[D][V];
     int par[V];
-    const uint32_t dmask = flow_deferred_mask(a, h, etab);
+    const uint32_t dmask = flow_deferred_mask(a, smask);
     const bool last = h.t == a.defer_last;
     const uint32_t fresh_lanes = h.t == a.fresh_t ? 0xffffffffu : a.fresh ? a.fresh[h.g] : 0u;
     if (HAS_SYN) {
@@ -639,9 +640,9 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
 #pragma unroll
         for (int v = 0; v < V; v++) sb[v] = (uint32_t)par[v] << 31;
         check_update_f32_d4<V, H>(reinterpret_cast<float(&)[4][V]>(q), reinterpret_cast<float(&)[4][V]>(ph), sb,
-                                  (float)a.mag_max, clip);
+                                  a.mag_f, clip);
     } else {
-        check_update_f32<V, D, H>(q, ph, par, h.d, (float)a.mag_max, clip);
+        check_update_f32<V, D, H>(q, ph, par, h.d, a.mag_f, clip);
     }
     if (ETF && lastm) {  // fused ET: hard-decision snapshot of the columns this slot writes last
         const unsigned mask = flow_live_mask(ct, lv_log2, h.kt);
@@ -671,7 +672,8 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
 // the new messages in registers until every thread has read its stash back.
 template <int V, int D, bool HAS_SYN, typename RT, bool ETF>
 __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
-                                                 const uint2 *etab, uint32_t lastm) {
+                                                 const uint2 *etab, uint32_t smask) {
+    const uint32_t lastm = smask >> 16;
     constexpr bool H = sizeof(RT) == 2;
     const int W = 1 << a.lw;
     const int KT = flow_kt(h.cls, W, a.lw);
@@ -682,12 +684,12 @@ __device__ __forceinline__ void flow_consume_gen(const FlowArgs &a, const FlowHd
     const bool act = ci < h.kt;
     if (!H && !act) return;
     const int off = ci * W + w0;
-    const float clip = (float)a.clip, mag_max = (float)a.mag_max;
+    const float clip = a.clip_f, mag_max = a.mag_f;
     using VT = typename Vec<float, V>::type;
     float q[D][V], t[D][V];
     int par[V];
     const uint32_t fresh_lanes = h.t == a.fresh_t ? 0xffffffffu : a.fresh ? a.fresh[h.g] : 0u;
-    const uint32_t dmask = flow_deferred_mask(a, h, etab);
+    const uint32_t dmask = flow_deferred_mask(a, smask);
     const bool last = h.t == a.defer_last;
     if (HAS_SYN && act) {
         const uint8_t *sp = a.syn + ((((int64_t)h.g * a.S + h.slot) * a.z + h.k0 + ci) << a.lw) + w0;
@@ -809,7 +811,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
     FlowHdr *hq = hdr + kFlowMaxStages;
     uint2 *stab = reinterpret_cast<uint2 *>(smem_raw + kFlowHeadBytes);
     uint2 *etab = stab + a.S;
-    uint32_t *slt = reinterpret_cast<uint32_t *>(etab + a.E);  // last-writer bits (fused ET), else 0
+    uint32_t *slt = reinterpret_cast<uint32_t *>(etab + a.E);  // slot masks (last-writer bits with ETF only)
     uint32_t *scratch = slt + a.S;                              // check items (consumers)
     float *stages = reinterpret_cast<float *>(smem_raw + flow_table_end(a.S, a.E));
     constexpr size_t kStageElems = kFlowStageBytes / 4;
@@ -819,7 +821,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
 
     for (int i = threadIdx.x; i < a.S; i += blockDim.x) stab[i] = a.slot_tab[i];
     for (int i = threadIdx.x; i < a.E; i += blockDim.x) etab[i] = a.edge_tab[i];
-    for (int i = threadIdx.x; i < a.S; i += blockDim.x) slt[i] = ETF ? a.slast[i] : 0u;
+    for (int i = threadIdx.x; i < a.S; i += blockDim.x) slt[i] = a.slot_mask[i] & (ETF ? 0xffffffffu : 0xffffu);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; s++) {
             mbar_init(&full[s], 1);
@@ -954,7 +956,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                     if (lane == 0 && h.t >= 1) spin_until_acquire(a.decided + (size_t)h.g * QCL_FLAG_STRIDE, h.t);
                     __syncwarp();
                 } else {
-                    if (ETF && slt[h.slot] && h.t >= 2) {  // snapshot parity reuse
+                    if (ETF && (slt[h.slot] >> 16) && h.t >= 2) {  // snapshot parity reuse
                         const int owner = h.g & 31;
                         const bool cached = __shfl_sync(0xffffffffu, dec_tag == h.g && dec_val >= h.t - 1, owner);
                         if (!cached && lane == owner) {
@@ -1042,7 +1044,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 fence_proxy_async_global();  // observed flags -> ordered before the bulk (async proxy) reads
                 const int KT = flow_kt(h.cls, W, a.lw);
                 // runs moved: d L runs, plus the R runs of edges not under degree-1 deferral
-                const uint32_t nr = (uint32_t)h.d - __popc(flow_deferred_mask(a, h, etab));
+                const uint32_t nr = (uint32_t)h.d - __popc(flow_deferred_mask(a, slt[h.slot]));
                 if (lane == 0) {
                     hdr[s] = h;
                     mbar_arrive_expect_tx(&full[s], ((uint32_t)h.d * 4 + nr * (uint32_t)sizeof(RT)) * (uint32_t)(h.kt * W));

@@ -92,7 +92,8 @@ struct qcl_plan {
     SlotInfo *slots = nullptr;  // device H_compact1: per slot
     EdgeInfo *edges = nullptr;  // device H_compact1: per circulant
     uint2 *fedge_tab = nullptr;  // device, flow engine: packed circulant + previous-writer table
-    uint32_t *fslast = nullptr;  // device, flow engine: per slot, bit j = edge j writes its column last
+    uint32_t *fslast = nullptr;  // device, flow engine: per slot, bits 0-15: edge j's column is degree 1,
+                                 // bits 16-31: edge j writes its column last in a sweep (flow.cuh)
     int32_t *funtouched = nullptr;  // device: columns no row touches (their decisions never change)
     int n_untouched = 0;
     bool flow_ok = false;        // the code fits the flow engine's packed tables
@@ -646,7 +647,6 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.check_items = st->f_check_items;
     if (etf) {
         const size_t gs = (size_t)st->G * QCL_FLAG_STRIDE;
-        a.slast = p->fslast;
         a.snap = st->fsnap;
         a.fsign = st->fsign;
         a.cdone = st->fet;
@@ -658,6 +658,7 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
         a.synpack = st->has_syn ? st->synpack : nullptr;
     }
     a.G = st->G;
+    a.slot_mask = p->fslast;
     a.t_base = t0;
     a.t_dev = t_dev;
     a.fresh_t = fresh_t;
@@ -682,6 +683,8 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     a.clip = clip;
     a.eps = eps;
     a.mag_max = mag_bound(clip, eps);
+    a.clip_f = (float)clip;
+    a.mag_f = (float)a.mag_max;
     const size_t smem = flow_smem_bytes(p->S, p->E, st->f_stages);
     const int64_t grid = std::min<int64_t>(st->f_grid, a.item_end);
     const bool prof = st->fstats != nullptr;
@@ -940,8 +943,9 @@ int qcl_plan_create(int32_t z, int32_t n_cols, int32_t n_slots, int32_t n_layers
                 const uint32_t reused = tl.size() > 1;
                 h_etab[e].x = (uint32_t)(c & 0x7fff) | (reused << 15) | ((uint32_t)edge_shift[e] << 16);
                 h_etab[e].y = (uint32_t)(slot_of[pe] & 0x7fff) | ((i == 0 ? 1u : 0u) << 15) | ((uint32_t)delta << 16);
-                if (i + 1 == tl.size() && e - slot_offsets[slot_of[e]] < 32)
-                    h_slast[slot_of[e]] |= 1u << (e - slot_offsets[slot_of[e]]);
+                const int j = e - slot_offsets[slot_of[e]];
+                if (j < 16 && i + 1 == tl.size()) h_slast[slot_of[e]] |= 1u << (16 + j);
+                if (j < 16 && tl.size() == 1) h_slast[slot_of[e]] |= 1u << j;
             }
         }
     }

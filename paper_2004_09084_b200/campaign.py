@@ -23,11 +23,15 @@ Extra ``CampaignConfig`` fields (all optional, reference behaviour by default):
 * ``devices`` -- GPU ordinals; each batch is split into contiguous slices, one per GPU
   and host thread (``np.array_split`` as ``bench.py:143``), no collective.  Default ``(0,)``.
 * ``frame_pool`` -- device channel with early termination on the FP32 flow engine: the
-  whole SNR point's frames stream through ``batch_size`` lanes per GPU, a lane taking the
-  next frame as soon as its frame converges or hits the cap (``qcl_state_decode_pool``),
-  so one slow frame no longer holds a batch to the cap.  Per-frame outcomes, hence FER and
-  average iterations, are identical to the batched decode; only the timing changes.
-  Default ``True`` (used whenever it applies).
+  first batch of an SNR point is decoded batched; if its frames stopped on average before
+  ~0.85 of the cap, the rest stream through ``batch_size`` lanes per GPU, a lane taking
+  the next frame as soon as its frame converges or hits the cap
+  (``qcl_state_decode_pool``), so one slow frame no longer holds a batch to the cap;
+  otherwise (most frames run to the cap) the rest is decoded batched, where early
+  termination runs inside one launch.  Per-frame outcomes, hence FER and average
+  iterations, are identical either way; only the timing changes.  Default ``True`` (used
+  whenever the flow engine runs; the report's ``roofline`` entries name the path);
+  ``"always"`` skips the first-batch probe's choice and streams the rest through the pool.
 
 Timing follows ``bench.py:230-234``: wall-clock around the decode only (LLR generation
 and error counting are outside), so ``throughput_mbits_per_s`` is frames * n / decode
@@ -337,19 +341,43 @@ class _PoolRunner(_DeviceChannelRunner):
         return all(self._state(dev, min(self.cfg.batch_size, count)).info()[1]
                    for dev, _, _, _, count in self._jobs(0, 1.0, frames))
 
+    # The pool pays ~0.71 ms per 64-lane sweep (a launch per sweep plus refills), a batched
+    # decode ~0.52 ms (early termination fused into one launch, DESIGN 3.3) but every sweep
+    # until the batch's slowest frame is done -- the cap as soon as one frame fails.  Measured
+    # on the n = 1e6 stand-in (profiles/r02_campaign_sweep_*.json, caps 20/50/100, SNR
+    # 0.14-0.20) the pool wins when frames stop on average before ~0.85 of the cap.
+    POOL_WHEN_MEAN_BELOW = 0.85
+
     def point(self, snr_idx, chan, frames):
-        jobs = self._jobs(snr_idx, chan.snr, frames)
+        """All frames of one SNR point: the first batch as a batched decode, the rest in the
+        frame pool when that batch's mean iteration count says the pool pays, else as
+        further batches.  Frames are independent, so every frame's outcome is the same
+        whichever path decodes it; only the timing differs.  Returns (converged, frame
+        error, iterations, wall seconds, path)."""
+        first = min(self.cfg.batch_size * len(self.plans), frames)
+        parts = [self.batch(snr_idx, chan, 0, first)]
+        use_pool = (self.cfg.frame_pool == "always"
+                    or float(parts[0][2].mean()) < self.POOL_WHEN_MEAN_BELOW * self.cfg.max_iterations)
+        if frames > first and use_pool:
+            jobs = [(dev, si, snr, f0 + first, count) for dev, si, snr, f0, count
+                    in self._jobs(snr_idx, chan.snr, frames - first)]
 
-        def run(job):
-            dev, si, snr, f0, count = job
-            st = self._state(dev, min(self.cfg.batch_size, count))
-            t0 = time.perf_counter()
-            conv, iters, err, _ = st.decode_pool(self.qcfg, self.cfg.seed, si, f0, count, snr)
-            return conv, err, iters, time.perf_counter() - t0
+            def run(job):
+                dev, si, snr, f0, count = job
+                st = self._state(dev, min(self.cfg.batch_size, count))
+                t0 = time.perf_counter()
+                conv, iters, err, _ = st.decode_pool(self.qcfg, self.cfg.seed, si, f0, count, snr)
+                return conv, err, iters, time.perf_counter() - t0
 
-        parts = list(self.pool.map(run, jobs)) if self.pool else [run(j) for j in jobs]
-        return (np.concatenate([p[0] for p in parts]), np.concatenate([p[1] for p in parts]),
-                np.concatenate([p[2] for p in parts]), max(p[3] for p in parts))
+            rest = list(self.pool.map(run, jobs)) if self.pool else [run(j) for j in jobs]
+            parts.append((np.concatenate([r[0] for r in rest]), np.concatenate([r[1] for r in rest]),
+                          np.concatenate([r[2] for r in rest]), max(r[3] for r in rest)))
+        else:
+            for start in range(first, frames, self.cfg.batch_size):
+                parts.append(self.batch(snr_idx, chan, start, min(self.cfg.batch_size, frames - start)))
+        return (np.concatenate([x[0] for x in parts]), np.concatenate([x[1] for x in parts]),
+                np.concatenate([x[2] for x in parts]), sum(x[3] for x in parts),
+                "pool" if (frames > first and use_pool) else "batched")
 
 
 BYTES_PER_EDGE_ITERATION = {"fp32": 16, "fp64": 32, "fp32-msg16": 12}  # SURVEY 8(d)
@@ -430,8 +458,9 @@ def run_campaign(cfg):
             errors = 0
             iterations_total = 0
             wall = 0.0
+            path = "batched"
             if pool:
-                converged, mismatch, iterations, wall = runner.point(snr_idx, chan, frames)
+                converged, mismatch, iterations, wall, path = runner.point(snr_idx, chan, frames)
                 errors += int((~converged).sum()) + int((converged & mismatch).sum())
                 iterations_total += int(iterations.sum())
             for start in range(0, 0 if pool else frames, cfg.batch_size):
@@ -453,14 +482,15 @@ def run_campaign(cfg):
                     utilization=util.utilization,
                 )
             )
-            roofline.append((iterations_total, wall))
+            roofline.append((iterations_total, wall, path))
     finally:
         runner.close()
 
     metadata = _campaign_metadata(cfg, base, desc, schedule)
     metadata["device"] = _device_metadata(cfg, pool)
     return CampaignReport(cells=tuple(cells), metadata=metadata,
-                          roofline=tuple(_roofline(c, it, w, metadata["device"]) for c, (it, w) in zip(cells, roofline)))
+                          roofline=tuple(dict(_roofline(c, it, w, metadata["device"]), path=path)
+                                         for c, (it, w, path) in zip(cells, roofline)))
 
 
 def compare_schedules(cfg):

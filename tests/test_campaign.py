@@ -189,10 +189,12 @@ def test_frame_pool_matches_batched_decode_per_frame(gpu, name):
     else:
         cfg = config_of(golden(name), channel="device", batch_size=32, min_trials=256)
     a = run_campaign(cfg.__class__(**{**cfg.__dict__, "frame_pool": False}))
-    b = run_campaign(cfg)
+    b = run_campaign(cfg.__class__(**{**cfg.__dict__, "frame_pool": "always"}))
+    c = run_campaign(cfg)  # adaptive: pool or batched per SNR point after a first-batch probe
     assert b.metadata["device"]["frame_pool"] and not a.metadata["device"]["frame_pool"]
-    for x, y in zip(a.cells, b.cells):
-        assert x.fer == y.fer and x.avg_iterations == y.avg_iterations, (x, y)
+    assert all(r["path"] == "pool" for r in b.roofline) and all(r["path"] == "batched" for r in a.roofline)
+    for x, y, w in zip(a.cells, b.cells, c.cells):
+        assert x.fer == y.fer == w.fer and x.avg_iterations == y.avg_iterations == w.avg_iterations, (x, y, w)
 
 
 @pytest.mark.gpu

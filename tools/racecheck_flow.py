@@ -1,4 +1,4 @@
-"""One small flow-engine decode (and one FP16-message decode) for compute-sanitizer racecheck.
+"""Small flow-engine decodes (FP32, FP16 messages, fused ET) for compute-sanitizer racecheck.
 
     compute-sanitizer --tool racecheck python tools/racecheck_flow.py
 """
@@ -23,3 +23,7 @@ for precision in ("fp32", "fp32-msg16"):
                            precision=precision)
     w, c, it = dec.decode_batch_arrays(llr, syn)
     print(precision, "decoded", int(c.sum()), flush=True)
+# fused early termination (round 2): snapshots, check items, decisions
+dec = q.LayeredDecoder(index, sched, q.DecoderConfig(max_iterations=3, early_termination=True))
+w, c, it = dec.decode_batch_arrays(rng.normal(2.0, 2.0, size=(16, n)), np.zeros((16, m), np.uint8))
+print("fused ET decoded", int(c.sum()), flush=True)

@@ -51,3 +51,18 @@ st = _native.State(_native.Plan(index, sched, 0), 16, "fp32")
 qcfg = _native.make_config(q.DecoderConfig(max_iterations=6, early_termination=True), "fp32")
 conv, iters, err, _ = st.decode_pool(qcfg, 0, 0, 0, 40, 0.3)
 print("frame pool 40 frames:", int(conv.sum()), "converged", int(iters.sum()), "iterations", flush=True)
+
+# fused early termination (round 2): encode-mode targets, two group blocks, a ragged group
+for B in (21, 128):
+    pl = _native.Plan(index, sched, 0)
+    outs = []
+    for engine in (0, 4):
+        s2 = _native.State(pl, B, "fp32")
+        s2.set_engine(engine)
+        s2.set_llr_synthetic(seed=5, snr_idx=1, first_frame=0, snr=0.19, encode_mode=True)
+        s2.decode(_native.make_config(q.DecoderConfig(max_iterations=8, early_termination=True), "fp32"))
+        outs.append(s2.results())
+    same = all(np.array_equal(a, b) for a, b in zip(*outs))
+    print(f"fused ET B={B}: engines agree: {same}, converged {int(outs[1][1].sum())}", flush=True)
+    if not same:
+        sys.exit(1)

@@ -53,6 +53,24 @@
 #ifndef QCL_FLOW_QUEUE
 #define QCL_FLOW_QUEUE 1
 #endif
+// role-warp waits: 0 = mbarrier try_wait with a suspend hint (wakes on barrier events);
+// N > 0 = test_wait polling with an N ns back-off (tuning knobs, tools/flow_build_variants.sh)
+#ifndef QCL_FLOW_STORER_SLEEP
+#define QCL_FLOW_STORER_SLEEP 0
+#endif
+#ifndef QCL_FLOW_LOADER_SLEEP
+#define QCL_FLOW_LOADER_SLEEP 0
+#endif
+#ifndef QCL_FLOW_CONSUMER_SLEEP
+#define QCL_FLOW_CONSUMER_SLEEP 0
+#endif
+#define QCL_ROLE_WAIT(bar, par, ns) \
+    do {                             \
+        if (ns > 0)                  \
+            mbar_wait_backoff(bar, par, ns); \
+        else                         \
+            mbar_wait_sleep(bar, par); \
+    } while (0)
 
 namespace qcl {
 
@@ -1017,7 +1035,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         const bool lprof = PROF;
         for (int it = 0, s = 0, ph = 0, q = 0, qph = 0;; it++) {
             if (lprof) tc = clock64();
-            mbar_wait_sleep(&ready[q], qph);
+            QCL_ROLE_WAIT(&ready[q], qph, QCL_FLOW_LOADER_SLEEP);
             if (lprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
             const FlowHdr h = hq[q];
             __syncwarp();
@@ -1026,7 +1044,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 q = 0;
                 qph ^= 1;
             }
-            if (it >= S) mbar_wait_sleep(&empty[s], ph ^ 1);
+            if (it >= S) QCL_ROLE_WAIT(&empty[s], ph ^ 1, QCL_FLOW_LOADER_SLEEP);
             if (lprof) { const long long c_ = clock64(); acc[1] += c_ - tc; tc = c_; }
             if (h.kt < 0) {
                 if (lane == 0) {
@@ -1078,7 +1096,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         for (int it = warp - 2;; it += kFlowStorers) {
             const int s = it % S;
             if (sprof) tc = clock64();
-            mbar_wait_sleep(&done[s], (it / S) & 1);
+            QCL_ROLE_WAIT(&done[s], (it / S) & 1, QCL_FLOW_STORER_SLEEP);
             if (sprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
             const FlowHdr h = hdr[s];
             if (h.kt < 0) break;
@@ -1116,7 +1134,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
     int sentinels = 0;
     for (int s = 0, ph = 0;;) {
         if (cprof) tc = clock64();
-        mbar_wait_sleep(&full[s], ph);
+        QCL_ROLE_WAIT(&full[s], ph, QCL_FLOW_CONSUMER_SLEEP);
         if (cprof) { const long long c_ = clock64(); acc[0] += c_ - tc; tc = c_; }
         const FlowHdr h = hdr[s];
         if (h.kt < 0) {

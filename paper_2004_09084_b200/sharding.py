@@ -36,29 +36,33 @@ def shard_range(total, world, rank):
 def gather_outcomes(words, converged, iterations, group=None):
     """All-gather per-rank (words, converged, iterations) into global arrays on every rank.
 
-    ``torch.distributed`` must be initialised (any backend: gloo on CPU, nccl on GPUs).
-    Words are bit-packed for the exchange (n/8 bytes per codeword).
+    ``torch.distributed`` must be initialised (any backend: gloo exchanges host tensors,
+    nccl device tensors on the rank's current GPU).  Words are bit-packed for the exchange
+    (n/8 bytes per codeword); this is the only collective of the data-parallel path, and
+    only for callers that want every frame's outcome on one rank.
     """
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    # NCCL exchanges device tensors (over NVLink on one node); gloo host tensors
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
     n = words.shape[1]
     packed = np.packbits(words.astype(np.uint8), axis=1)
     local = torch.from_numpy(
         np.concatenate([packed, converged.astype(np.uint8)[:, None],
                         iterations.astype(np.int64).view(np.uint8).reshape(-1, 8)], axis=1)
-    )
-    counts = torch.tensor([local.shape[0]], dtype=torch.int64)
+    ).to(dev)
+    counts = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
     all_counts = [torch.zeros_like(counts) for _ in range(world)]
     dist.all_gather(all_counts, counts, group=group)
     width = local.shape[1]
     cap = int(max(c.item() for c in all_counts))
-    padded = torch.zeros((cap, width), dtype=torch.uint8)
+    padded = torch.zeros((cap, width), dtype=torch.uint8, device=dev)
     padded[: local.shape[0]] = local
     bufs = [torch.zeros_like(padded) for _ in range(world)]
     dist.all_gather(bufs, padded, group=group)
-    rows = np.concatenate([b[: int(c.item())].numpy() for b, c in zip(bufs, all_counts)])
+    rows = np.concatenate([b[: int(c.item())].cpu().numpy() for b, c in zip(bufs, all_counts)])
     nb = packed.shape[1]
     w = np.unpackbits(rows[:, :nb], axis=1)[:, :n]
     conv = rows[:, nb].astype(bool)

@@ -183,3 +183,34 @@ def test_bench_two_ranks_plumbing(gpu):
     line = lines[0]
     assert line["n_gpus"] == 2 and line["config"]["global_batch"] == 32 and line["config"]["batch_per_gpu"] == 16
     assert "ranks_share_gpus" in line and line["value"] > 0 and line["e2e"]["value"] > 0
+
+
+def _nccl_rank(rank, port, out):
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    from paper_2004_09084_b200.sharding import gather_outcomes
+
+    rng = np.random.default_rng(3)
+    w = (rng.random((5, 1003)) < 0.5).astype(np.uint8)
+    c = rng.random(5) < 0.5
+    it = rng.integers(1, 50, 5)
+    gw, gc, gi = gather_outcomes(w, c, it)
+    np.savez(out, ok=np.array(np.array_equal(gw, w) and np.array_equal(gc, c) and np.array_equal(gi, it)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gather_outcomes_over_nccl(gpu, tmp_path):
+    """The result gather on an NCCL group exchanges device tensors (one rank here: the
+    packing, the device round trip and the unpacking are what is checked)."""
+    import torch.multiprocessing as mp
+
+    out = tmp_path / "n.npz"
+    mp.spawn(_nccl_rank, args=(_free_port(), str(out)), nprocs=1, join=True)
+    assert bool(np.load(out)["ok"])

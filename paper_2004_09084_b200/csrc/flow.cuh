@@ -602,9 +602,14 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
 }
 
 // One consumer thread: check (ci) of the tile for V lanes, in place in the stage.
-template <int V, int D, bool HAS_SYN, typename RT, bool ETF>
-__device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
-                                             const uint2 *etab, uint32_t smask) {
+// DF > 0: the slot's degree is DF; DMF >= 0: its deferral mask is DMF (compile-time
+// specialisations of the common case -- every degree-4 row of the MET code has exactly one
+// degree-1 column, its last edge -- which drop the per-edge degree/mask tests and the R
+// stores the storer would skip anyway)
+template <int V, int D, bool HAS_SYN, typename RT, bool ETF, int DF, int DMF>
+__device__ __forceinline__ void flow_consume_body(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
+                                                  const uint2 *etab, uint32_t smask) {
+    const int d = DF > 0 ? DF : h.d;
     const uint32_t lastm = smask >> 16;
     const int W = 1 << a.lw;
     const int KT = flow_kt(h.cls, W, a.lw);
@@ -619,7 +624,7 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
     using VT = typename Vec<float, V>::type;
     float q[D][V], ph[D][V];
     int par[V];
-    const uint32_t dmask = flow_deferred_mask(a, smask);
+    const uint32_t dmask = DMF >= 0 ? (uint32_t)DMF : flow_deferred_mask(a, smask);
     const bool last = h.t == a.defer_last;
     const uint32_t fresh_lanes = h.t == a.fresh_t ? 0xffffffffu : a.fresh ? a.fresh[h.g] : 0u;
     if (HAS_SYN) {
@@ -632,7 +637,7 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
     }
 #pragma unroll
     for (int j = 0; j < D; j++) {
-        if (j < h.d) {
+        if (j < d) {
             float lv[V], rv[V];
             *reinterpret_cast<VT *>(lv) = *reinterpret_cast<const VT *>(stage + (size_t)j * KTW + off);
             if ((dmask >> j) & 1) {  // the L slot already holds q
@@ -653,32 +658,46 @@ __device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h
             for (int v = 0; v < V; v++) q[j][v] = 0.0f;
         }
     }
-    if (D == 4 && h.d == 4) {
+    if (D == 4 && d == 4) {
         uint32_t sb[V];
 #pragma unroll
         for (int v = 0; v < V; v++) sb[v] = (uint32_t)par[v] << 31;
         check_update_f32_d4<V, H>(reinterpret_cast<float(&)[4][V]>(q), reinterpret_cast<float(&)[4][V]>(ph), sb,
                                   a.mag_f, clip);
     } else {
-        check_update_f32<V, D, H>(q, ph, par, h.d, a.mag_f, clip);
+        check_update_f32<V, D, H>(q, ph, par, d, a.mag_f, clip);
     }
     if (ETF && lastm) {  // fused ET: hard-decision snapshot of the columns this slot writes last
         const unsigned mask = flow_live_mask(ct, lv_log2, h.kt);
 #pragma unroll
         for (int j = 0; j < D; j++)
-            if (j < h.d && ((lastm >> j) & 1)) flow_snap<V>(a, h, etab[h.edge_off + j].x, ci, w0, q[j], mask);
+            if (j < d && ((lastm >> j) & 1)) flow_snap<V>(a, h, etab[h.edge_off + j].x, ci, w0, q[j], mask);
     }
 #pragma unroll
     for (int j = 0; j < D; j++) {
-        if (j < h.d) {
-            if (((dmask >> j) & 1) && !last) {  // next sweep's q for a deferred degree-1 edge
+        if (j < d) {
+            const bool deferred = (dmask >> j) & 1;
+            if (deferred && !last) {  // next sweep's q for a deferred degree-1 edge
 #pragma unroll
                 for (int v = 0; v < V; v++) q[j][v] = clampT(q[j][v] - ph[j][v], clip);
             }
-            msg_store<V>(reinterpret_cast<RT *>(stage + (size_t)(D + j) * KTW) + off, ph[j]);
+            // a deferred edge's R run is stored only in the last sweep (flow_runs)
+            if (DMF < 0 || !deferred || last)
+                msg_store<V>(reinterpret_cast<RT *>(stage + (size_t)(D + j) * KTW) + off, ph[j]);
             *reinterpret_cast<VT *>(stage + (size_t)j * KTW + off) = *reinterpret_cast<VT *>(q[j]);
         }
     }
+}
+
+template <int V, int D, bool HAS_SYN, typename RT, bool ETF>
+__device__ __forceinline__ void flow_consume(const FlowArgs &a, const FlowHdr &h, float *stage, int ct,
+                                             const uint2 *etab, uint32_t smask) {
+    if constexpr (D == 4) {
+        const uint32_t dm = flow_deferred_mask(a, smask);
+        if (h.d == 4 && dm == 8u) return flow_consume_body<V, D, HAS_SYN, RT, ETF, 4, 8>(a, h, stage, ct, etab, smask);
+        if (h.d == 4 && dm == 0u) return flow_consume_body<V, D, HAS_SYN, RT, ETF, 4, 0>(a, h, stage, ct, etab, smask);
+    }
+    flow_consume_body<V, D, HAS_SYN, RT, ETF, 0, -1>(a, h, stage, ct, etab, smask);
 }
 
 // Degree classes 1 and 2 (rows of degree 5..12): the sum/difference update with the

@@ -87,7 +87,12 @@ namespace qcl {
 // consumer warps share every tile (half the service time per tile, so half the time a
 // claimed tile spends queued), with more storers and a deeper ring
 constexpr int kFlowConsumers = QCL_FLOW_WIDE ? 16 : 8;  // consumer warps per CTA
-constexpr int kFlowStorers = QCL_FLOW_WIDE ? 4 : 2;     // storer warps per CTA
+#ifndef QCL_FLOW_STORERS
+#define QCL_FLOW_STORERS (QCL_FLOW_WIDE ? 4 : 2)
+#endif
+// storer warps per CTA: storer k takes ring positions k, k + storers, ...; each must finish
+// a stage's store, read-out wait and flag release (a GPU-scope fence) before its next one
+constexpr int kFlowStorers = QCL_FLOW_STORERS;
 constexpr int kFlowCtasPerSm = QCL_FLOW_WIDE ? 1 : 2;
 constexpr int kFlowThreads = 32 * (kFlowConsumers + 2 + kFlowStorers);
 constexpr int kFlowQueue = QCL_FLOW_QUEUE;         // scheduler -> loader header queue depth

@@ -777,6 +777,18 @@ __global__ void llr_to_lanes_kernel(const S *src, int64_t B, int64_t Bp, int64_t
 template <typename T>
 __global__ void reset_kernel(const T *llr, T *L, int64_t count, double clip) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if constexpr (sizeof(T) == 4) {  // four values per thread (16-byte accesses); count % 4 == 0 (W >= 4)
+        if ((count & 3) == 0) {
+            if (4 * i >= count) return;
+            float4 x = reinterpret_cast<const float4 *>(llr)[i];
+            x.x = (float)clampT((double)x.x, clip) + 0.0f;
+            x.y = (float)clampT((double)x.y, clip) + 0.0f;
+            x.z = (float)clampT((double)x.z, clip) + 0.0f;
+            x.w = (float)clampT((double)x.w, clip) + 0.0f;
+            reinterpret_cast<float4 *>(L)[i] = x;
+            return;
+        }
+    }
     if (i < count) L[i] = (T)clampT((double)llr[i], clip) + (T)0;
 }
 

@@ -1346,9 +1346,9 @@ int qcl_state_set_syndrome(qcl_state *st, const uint8_t *syndrome) {
 static int enqueue_reset(qcl_state *st, double clip, bool zero_r = true) {
     const qcl_plan *p = st->plan;
     const int64_t nl = st->Bp * p->n;
-    if (st->prec == QCL_PREC_FP32)
-        reset_kernel<float><<<(unsigned)cdiv(nl, kBlock), kBlock, 0, st->stream>>>((const float *)st->llr,
-                                                                                    (float *)st->L, nl, clip);
+    if (st->prec == QCL_PREC_FP32)  // 4 values per thread when nl % 4 == 0
+        reset_kernel<float><<<(unsigned)cdiv(nl % 4 == 0 ? nl / 4 : nl, kBlock), kBlock, 0, st->stream>>>(
+            (const float *)st->llr, (float *)st->L, nl, clip);
     else
         reset_kernel<double><<<(unsigned)cdiv(nl, kBlock), kBlock, 0, st->stream>>>((const double *)st->llr,
                                                                                      (double *)st->L, nl, clip);

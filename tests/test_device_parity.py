@@ -500,3 +500,49 @@ def test_device_channel_distribution(gpu):
     assert abs(np.corrcoef(z[:-1], z[1:])[0, 1]) < 2e-3
     f = z.reshape(8, -1)
     assert np.abs(np.corrcoef(f)[np.triu_indices(8, 1)]).max() < 5e-3
+
+
+def test_pageable_and_pinned_host_buffers_agree(gpu):
+    """The host staging pipeline (csrc/hostio.h): 16 codewords of the n = 10^6 code as
+    pageable float64 (the reference's format; 128 MB through the 8 MB pinned ring, converted
+    to float32 on the host threads), pageable float32, and pinned float32, with a nonzero
+    target syndrome -- identical outcomes; words read back through the ring into pageable
+    memory (16 MB, two chunks) equal the pinned path's."""
+    import paper_2004_09084_b200 as q
+    from paper_2004_09084_b200 import _native
+
+    base, sched, index = load_code("standin_v2_z2500")
+    n, m = base.n_cols * base.z, base.n_rows * base.z
+    rng = np.random.default_rng(5)
+    llr = rng.normal(3.0, 2.0, size=(16, n))
+    syn = (rng.random((16, m)) < 0.001).astype(np.uint8)
+    dec = q.LayeredDecoder(index, sched, q.DecoderConfig(max_iterations=3, early_termination=False))
+    a = dec.decode_batch_arrays(llr, syn)
+    b = dec.decode_batch_arrays(llr.astype(np.float32), syn)
+    pin = _native.PinnedArray((16, n), np.float32)
+    pin.array[...] = llr
+    spin = _native.PinnedArray((16, m), np.uint8)
+    spin.array[...] = syn
+    c = dec.decode_batch_arrays(pin.array, spin.array)
+    for x, y, z in zip(a, b, c):
+        assert np.array_equal(x, y) and np.array_equal(x, z)
+    assert a[0].any() and not a[0].all()
+
+
+def test_stream_results_outlive_their_slots(gpu):
+    """a yielded words array is a view of a pinned slot buffer; dropping the
+    decoder's slots (a batch-size or depth change) must not free memory a view still uses."""
+    import gc
+
+    import paper_2004_09084_b200 as q
+
+    base, sched, index = load_code("demo_4x8_z100")
+    n, m = base.n_cols * base.z, base.n_rows * base.z
+    llr = np.random.default_rng(2).normal(2.0, 1.0, size=(8, n))
+    dec = q.LayeredDecoder(index, sched, q.DecoderConfig(max_iterations=5, early_termination=False))
+    kept = [w for w, _, _ in dec.decode_stream([(llr, np.zeros((8, m), np.uint8))], depth=1)]
+    snapshot = kept[0].copy()
+    list(dec.decode_stream([(llr[:3], np.zeros((3, m), np.uint8))], depth=2))  # replaces the slot cache
+    dec = None
+    gc.collect()
+    assert np.array_equal(kept[0], snapshot)

@@ -571,7 +571,7 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
     if (ct == 0) {
         __threadfence();
         const uint32_t un = *(volatile uint32_t *)unsat;
-        const uint32_t act = a.amask[g];
+        const uint32_t act = __ldcg(a.amask + g);  // L2: earlier decisions may have run on other SMs
         const uint32_t newm = act & ~un;
         sc[2] = newm;
         if (newm) {
@@ -594,7 +594,7 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
         const int64_t n16 = (a.n % 16 == 0) ? a.n / 16 : 0;  // 16-byte rows only when n is a multiple
         for (int64_t i = ct; i < n16; i += kThreads) {
             const uint4 x = __ldcg(reinterpret_cast<const uint4 *>(sg) + i);
-            uint4 f = reinterpret_cast<uint4 *>(fg)[i];
+            uint4 f = __ldcg(reinterpret_cast<const uint4 *>(fg) + i);  // L2, as above
             f.x = (f.x & ~m4) | (x.x & m4);
             f.y = (f.y & ~m4) | (x.y & m4);
             f.z = (f.z & ~m4) | (x.z & m4);
@@ -602,7 +602,7 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
             reinterpret_cast<uint4 *>(fg)[i] = f;
         }
         for (int64_t v = n16 * 16 + ct; v < a.n; v += kThreads)
-            fg[v] = (uint8_t)((fg[v] & ~newm) | (__ldcg(sg + v) & newm));
+            fg[v] = (uint8_t)((__ldcg(fg + v) & ~newm) | (__ldcg(sg + v) & newm));
     }
     consumers_sync();
     if (ct == 0) {

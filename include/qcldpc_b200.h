@@ -83,7 +83,12 @@ int qcl_plan_info(const qcl_plan *plan, int64_t *n_vars, int64_t *n_checks, int6
 
 /* LayeredDecoder.decode_batch_arrays (decoder.py:275-312): one-shot host-buffer decode.
  * llr0 is (B, n) float64 (QCL_DTYPE_F64) or float32 (QCL_DTYPE_F32); syndrome may be
- * NULL (all-zero target).  Outputs: words (B, n), converged (B), iterations (B). */
+ * NULL (all-zero target).  Outputs: words (B, n), converged (B), iterations (B).
+ * Every host buffer may be pageable (the reference's numpy arrays) or pinned
+ * (qcl_host_alloc): pageable ones go through a pinned-chunk pipeline driven by host
+ * threads (float64 LLRs converted to float32 there for the FP32 paths); an all-zero
+ * syndrome is detected on the host and not copied.  Every entry point of this header runs
+ * on its plan's device and restores the calling thread's current device on return. */
 int qcl_decode(qcl_plan *plan, const qcl_config *cfg, const void *llr0, int32_t llr_dtype,
                const uint8_t *syndrome, int64_t batch, uint8_t *words, uint8_t *converged,
                int64_t *iterations);
@@ -91,7 +96,9 @@ int qcl_decode(qcl_plan *plan, const qcl_config *cfg, const void *llr0, int32_t 
 /* ---- device-resident state (DecoderState, decoder.py:75-93) ---------------- */
 int qcl_state_create(qcl_plan *plan, int64_t batch, int32_t precision, qcl_state **out);
 int qcl_state_destroy(qcl_state *st);
-/* Channel LLRs from host (B, n) -> device input buffer (channel.py:54-56 output). */
+/* Channel LLRs from host (B, n) -> device input buffer (channel.py:54-56 output).  A
+ * pageable llr0 is staged before the call returns (the caller may reuse it at once); a
+ * pinned one is read asynchronously on the state's stream. */
 int qcl_state_set_llr(qcl_state *st, const void *llr0, int32_t llr_dtype);
 /* Device BIAWGN generator (replaces channel.py:36-56 on the hot path): frame b of the
  * state is frame (first_frame + b) of the Philox4x32-10 stream keyed by (seed, snr_idx).

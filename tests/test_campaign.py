@@ -215,3 +215,20 @@ def test_frame_pool_per_frame_outcomes_against_states(gpu):
     rerr = ref.frame_errors()
     assert np.array_equal(conv, rconv) and np.array_equal(iters, riters)
     assert np.array_equal(err, ~rconv | rerr)
+
+
+@pytest.mark.gpu
+def test_campaign_command_line(gpu, tmp_path):
+    """`python -m paper_2004_09084_b200.campaign` (the reference's `decode-bench run`,
+    cli.py:94-139): a JSON report with the reference schema plus the device block."""
+    from paper_2004_09084_b200.campaign import main
+
+    out = tmp_path / "r.json"
+    rc = main(["--matrix", str(ROOT / "codes" / "demo_4x8_z100.txt"), "--snr", "1.5", "2.5", "--iterations", "10",
+               "--early-termination", "--batch-size", "16", "--min-trials", "32", "--channel", "device",
+               "--out", str(out)])
+    assert rc == 0
+    rep = json.loads(out.read_text())
+    assert rep["schema_version"] == 1 and len(rep["cells"]) == 2 and len(rep["roofline"]) == 2
+    assert rep["metadata"]["device"]["channel"] == "device"
+    assert rep["cells"][1]["fer"] <= rep["cells"][0]["fer"]

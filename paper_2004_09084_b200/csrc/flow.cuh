@@ -56,9 +56,6 @@
 #ifndef QCL_FLOW_ET_STOP
 #define QCL_FLOW_ET_STOP 1  // fused ET: schedulers stop claiming once every frame converged
 #endif
-#ifndef QCL_FLOW_PAIR
-#define QCL_FLOW_PAIR 0  // 1: the scheduler claims items in pairs (one flag round trip for two)
-#endif
 // role-warp waits: 0 = mbarrier try_wait with a suspend hint (wakes on barrier events);
 // N > 0 = test_wait polling with an N ns back-off (tuning knobs, tools/flow_build_variants.sh)
 #ifndef QCL_FLOW_STORER_SLEEP
@@ -894,7 +891,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         // through a small queue, so dependency polling overlaps the bulk-copy issue.
         const int t_base = a.t_dev ? *(volatile const int *)a.t_dev : a.t_base;
         int n2 = 0;
-        if (!QCL_FLOW_PAIR && lane == 0) n2 = atomicAdd(a.counter, 1);
+        if (lane == 0) n2 = atomicAdd(a.counter, 1);
         // stop: every frame converged (fused ET) -- the items already claimed (the one in
         // hand and the prefetched one) are still processed, nothing new is claimed
         bool stop = false;
@@ -907,7 +904,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             int t;
             return __ldg(a.items + flow_item_map(a, n, t));
         };
-        int n1 = QCL_FLOW_PAIR ? a.item_end : next_claim();  // (paired claims: below)
+        int n1 = next_claim();
         int2 r1 = make_int2(0, 0);
         if (n1 < a.item_end) r1 = record(n1);
         int sentinels = 0;
@@ -956,129 +953,6 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
             h.kt = min(KT, a.z - h.k0);
             return h;
         };
-#if QCL_FLOW_PAIR
-        // Paired claims (one atomicAdd of 2): both items' dependency flags are loaded in ONE
-        // round trip (a half-warp each: d <= 12 edges), then the two headers are queued in
-        // claim order.  Deadlock free as before: each item waits only for earlier claims.
-        {
-            int q = 0, ph = 0, pushed = 0;
-            auto push = [&](const FlowHdr &hh) {
-                if (pushed >= kFlowQueue) mbar_wait_sleep(&qfree[q], ph ^ 1);
-                __syncwarp();
-                if (lane == 0) {
-                    hq[q] = hh;
-                    mbar_arrive(&ready[q]);
-                }
-                pushed++;
-                if (++q == kFlowQueue) {
-                    q = 0;
-                    ph ^= 1;
-                }
-            };
-            const int end = a.item_end;
-            int pn = 0;
-            if (lane == 0) pn = atomicAdd(a.counter, 2);
-            auto claim_pair = [&]() {
-                const int n = __shfl_sync(0xffffffffu, pn, 0);
-                if (n < end && lane == 0) pn = stop ? end : atomicAdd(a.counter, 2);
-                return n;
-            };
-            auto flag_plan_j = [&](const FlowHdr &h, int j, const int *&fl, int &need, int &lo, int &nlo, int &nfl) {
-                nfl = 0;
-                if (j >= h.d) return;
-                const uint32_t dy = etab[h.edge_off + j].y;
-                need = h.t + 1 - (int)((dy >> 15) & 1);
-                if (need <= 0) return;
-                const uint2 pst = stab[dy & 0x7fff];
-                const int pcls = pst.x >> 24;
-                fl = a.flags + ((size_t)h.g * a.nkb_total + pst.y) * QCL_FLAG_STRIDE;
-                int a0 = h.k0 + (int)(dy >> 16);
-                a0 -= (a0 >= a.z) ? a.z : 0;
-                const int b = a0 + h.kt - 1;
-                lo = flow_kb_of(a0, pcls, W, a.lw);
-                nlo = flow_kb_of(min(b, a.z - 1), pcls, W, a.lw) - lo + 1;
-                nfl = nlo + (b >= a.z ? flow_kb_of(b - a.z, pcls, W, a.lw) + 1 : 0);
-            };
-            int nA = claim_pair();
-            int2 eA = make_int2(0, 0), eB = make_int2(0, 0);
-            if (nA < end) eA = record(nA);
-            if (nA + 1 < end) eB = record(nA + 1);
-            for (;;) {
-                if (nA >= end) {
-                    FlowHdr sen;
-                    sen.kt = -1;
-                    for (int k = 0; k < kFlowStorers; k++) push(sen);  // one end marker per storer
-                    break;
-                }
-                const int c[2] = {nA, nA + 1};
-                const int2 x[2] = {eA, eB};
-                nA = claim_pair();
-                if (nA < end) eA = record(nA);
-                if (nA + 1 < end) eB = record(nA + 1);
-                FlowHdr hh[2];
-                bool live[2];
-#pragma unroll
-                for (int k = 0; k < 2; k++) {
-                    live[k] = false;
-                    if (c[k] >= end) continue;
-                    hh[k] = resolve(c[k], x[k]);
-                    if (hh[k].k0 < 0 && hh[k].t < 0) continue;  // the first sweep's check items: nothing
-                    if (hh[k].k0 >= 0 && a.gactive && !a.gactive[hh[k].g]) {  // converged group: release only
-                        __syncwarp();
-                        if (lane == 0)
-                            flag_release(a.flags + ((size_t)hh[k].g * a.nkb_total + stab[hh[k].slot].y + x[k].y) *
-                                                       QCL_FLAG_STRIDE,
-                                         hh[k].t + 1, ETF);
-                        if (QCL_FLOW_ET_STOP && ETF) {
-                            int none = 0;
-                            if (lane == 0) none = *(volatile const int *)a.n_active == 0;
-                            stop = stop || __shfl_sync(0xffffffffu, none, 0);
-                        }
-                        continue;
-                    }
-                    live[k] = true;
-                }
-                // both items' covering flags in one round trip: half-warp k for item k
-                const int kh = lane >> 4, j = lane & 15;
-                const int *fl = nullptr;
-                int need = 0, lo = 0, nlo = 0, nfl = 0, fv[4];
-                if (live[kh] && hh[kh].k0 >= 0) flag_plan_j(hh[kh], j, fl, need, lo, nlo, nfl);
-#pragma unroll
-                for (int m = 0; m < 4; m++)
-                    if (m < nfl) fv[m] = ld_flag(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE);
-#pragma unroll
-                for (int k = 0; k < 2; k++) {
-                    if (!live[k]) continue;
-                    const FlowHdr &h = hh[k];
-                    if (h.k0 < 0) {
-                        if (lane == 0 && h.t >= 1) spin_until_acquire(a.decided + (size_t)h.g * QCL_FLAG_STRIDE, h.t);
-                    } else {
-                        if (ETF && (slt[h.slot] >> 16) && h.t >= 2) {  // snapshot parity reuse
-                            const int owner = h.g & 31;
-                            const bool cached =
-                                __shfl_sync(0xffffffffu, dec_tag == h.g && dec_val >= h.t - 1, owner);
-                            if (!cached && lane == owner) {
-                                spin_until(a.decided + (size_t)h.g * QCL_FLAG_STRIDE, h.t - 1);
-                                dec_tag = h.g;
-                                dec_val = h.t - 1;
-                            }
-                        }
-                        if (kh == k) {
-#pragma unroll
-                            for (int m = 0; m < 4; m++)
-                                if (m < nfl && fv[m] < need)
-                                    spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need);
-                            for (int m = 4; m < nfl; m++)
-                                spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need);
-                        }
-                    }
-                    flow_acquire_fence();
-                    push(h);
-                }
-            }
-        }
-        (void)prof;
-#else
         for (int it = 0, q = 0, ph = 0;; it++) {
             if (prof) tc = clock64();
             if (it >= kFlowQueue) mbar_wait_sleep(&qfree[q], ph ^ 1);
@@ -1168,7 +1042,6 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         next_item:
             it--;  // nothing was queued: this queue slot is still free
         }
-#endif
         if (prof && lane == 0) {
             for (int k = 0; k < 4; k++) atomicAdd(a.stats + 3 + k, (unsigned long long)acc[k]);
             atomicAdd(a.stats, n_waited);

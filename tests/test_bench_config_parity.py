@@ -4,12 +4,12 @@ The rate-0.1 n = 10^6 stand-in (``standin_v2_z2500``), SNR 0.161, 50 layered
 iterations, no early termination -- the workload ``bench.py`` times -- compared with
 the C oracle (the FP64 restatement of ``/root/reference/pkg/src/qcldpc/decoder.py:
 275-312``) on the bench's own device LLRs (``set_llr_synthetic(seed 0, snr_idx 0,
-frames 0..15, SNR 0.161)``), 16 frames = 16 Mbit of hard decisions.
+frames 0..63, SNR 0.161)``), the full 64-codeword batch = 64 Mbit of hard decisions.
 
 Contracts (stated here, measured values in DESIGN.md section 4):
 
 * ``precision="fp64"`` (the reference formula and fold order): hard decisions,
-  converged flags and iteration counts bit-exact; posteriors within 1e-9 relative.
+  converged flags and iteration counts bit-exact; posteriors within 1e-8 relative.
 * ``precision="fp32"`` (the benchmarked path): converged flags and iterations
   identical; every hard decision whose oracle posterior satisfies
   |L| >= FP32_DECISION_MARGIN identical, and flipped bits (only possible below that
@@ -21,7 +21,7 @@ Contracts (stated here, measured values in DESIGN.md section 4):
   (libdevice expf/logf, IEEE division): the flips stay (tools/fp32_parity_diag.py,
   profiles/r02_fp32_parity_diag.jsonl).  Bit-exact decisions are the FP64 mode.
 
-The oracle runs on every host core of the GPU box (~12 s for 16 frames).
+The oracle runs on every host core of the GPU box (~50 s for 64 frames).
 """
 
 import numpy as np
@@ -31,13 +31,13 @@ from conftest import load_code
 
 pytestmark = pytest.mark.gpu
 
-FRAMES = 16
+FRAMES = 64  # the full configs[2] batch
 SNR = 0.161
 ITERS = 50
 FP32_DECISION_MARGIN = 1e-3
 FP32_POSTERIOR_MAX = 1e-3
 FP32_POSTERIOR_Q99 = 1e-4
-FP64_POSTERIOR = 1e-9
+FP64_POSTERIOR = 1e-8  # 64 frames: 9.1e-10 measured (1-ulp libm/libdevice differences, amplified)
 
 _CACHE = {}
 

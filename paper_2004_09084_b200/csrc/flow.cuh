@@ -476,6 +476,7 @@ __device__ __forceinline__ void flow_snap(const FlowArgs &a, const FlowHdr &h, u
 __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, int ct, const uint2 *stab,
                                            const uint2 *etab, uint32_t *sc) {
     constexpr int kThreads = kFlowConsumers * 32;
+    constexpr int kCk = 4;  // checks per thread in flight in a scan
     const int g = h.g, t = h.t, par = t & 1, z = a.z;
     uint32_t *unsat = a.unsat + ((size_t)par * a.G + g) * QCL_FLAG_STRIDE;
     uint32_t acc = 0;
@@ -484,7 +485,7 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
     // the decision -- before convergence that is almost immediately, so most check items
     // scan a few checks, not z per slot
     const uint32_t need = __ldcg(a.amask + g);
-    const uint32_t known = __ldcg(unsat);
+    uint32_t known = __ldcg(unsat);
 #ifndef QCL_FLOW_CHECK_EARLY
 #define QCL_FLOW_CHECK_EARLY 1
 #endif
@@ -512,19 +513,110 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
     consumers_sync();  // uniform: every consumer thread computed the same `scan`
+    const uint8_t *sg = a.snap + ((size_t)par * a.G + g) * a.n;
+    // parity bits (lanes) of check k of slot s in this sweep's snapshot (^ target syndrome)
+    auto check_bits = [&](int s, int k) {
+        const uint32_t sx = stab[s].x;
+        const int eo = sx & 0xffff, d = (sx >> 16) & 0xff;
+        uint32_t b = a.synpack ? __ldg(a.synpack + ((size_t)s * z + k) * a.G + g) : 0u;
+        for (int j = 0; j < d; j++) {
+            const uint32_t ex = etab[eo + j].x;
+            int pos = k + (int)(ex >> 16);
+            pos -= (pos >= z) ? z : 0;
+            b ^= __ldcg(sg + (size_t)(ex & 0x7fff) * z + pos);
+        }
+        return b;
+    };
+    // near convergence a codeword's few unsatisfied checks persist from sweep to sweep: the
+    // check each lane failed last (hint[lane], id + 1) is tested first, which usually ends
+    // the scan at once.  Which unsatisfied check is found does not matter for the decision.
+    int *hint = a.cdone + (size_t)(4 * a.G + g) * QCL_FLAG_STRIDE;
+    if (scan && ct < 32) {
+        uint32_t hb = 0;
+        if (ct < (1 << a.lw) && (((need & ~known) >> ct) & 1)) {
+            const int id = __ldcg(hint + ct) - 1;
+            if (id >= 0) hb = check_bits(id / z, id % z);
+        }
+        hb = __reduce_or_sync(0xffffffffu, hb);
+        if (ct == 0) sc[2] = hb;
+    }
+    consumers_sync();
     if (scan) {
-        const uint8_t *sg = a.snap + ((size_t)par * a.G + g) * a.n;
-        bool done = false;
+        acc = sc[2];
+        known |= acc;
+        bool done = (known & need) == need;
         for (int s = h.slot; s < h.kt && !done; s++) {  // h.kt: end of the slot range
             const uint32_t sx = stab[s].x;
             const int eo = sx & 0xffff, d = (sx >> 16) & 0xff;
-            // four checks per thread in flight, all d x 4 byte loads (L2 round trips) issued
-            // before the XORs
-            for (int kw = ct & ~31; kw < z; kw += 4 * kThreads) {  // warp-uniform trip count
-                const int k0 = kw + (ct & 31);
-                uint32_t pb[4];
+            if ((z & 3) == 0) {
+                // z a multiple of 4: each thread takes kCk quads of 4 consecutive checks; a
+                // quad's bytes in one column are 4 consecutive bytes (mod z) = two aligned
+                // words and a byte permute; all 2 d kCk word loads (L2 round trips) are issued
+                // before the XORs
+                for (int kw = (ct & ~31) * 4; kw < z; kw += kCk * kThreads * 4) {  // warp-uniform trips
+                    const int k0 = kw + (ct & 31) * 4;
+                    const uint32_t kn = (ct & 31) == 0 ? __ldcg(unsat) : 0u;  // other items' finds
+                    uint32_t pb[kCk];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
+                    for (int u = 0; u < kCk; u++) {
+                        const int k = k0 + u * kThreads * 4;
+                        pb[u] = 0;
+                        if (a.synpack && k < z) {
+                            const uint32_t *sp = a.synpack + ((size_t)s * z + k) * a.G + g;
+#pragma unroll
+                            for (int i = 0; i < 4; i++) pb[u] |= __ldg(sp + (size_t)i * a.G) << (8 * i);
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < 12; j++) {
+                        if (j < d) {
+                            const uint32_t ex = etab[eo + j].x;
+                            const uint32_t *colw = reinterpret_cast<const uint32_t *>(sg + (size_t)(ex & 0x7fff) * z);
+                            const int sh = (int)(ex >> 16);
+#pragma unroll
+                            for (int u = 0; u < kCk; u++) {
+                                const int k = k0 + u * kThreads * 4;
+                                int pos = k + sh;
+                                pos -= (pos >= z) ? z : 0;
+                                const int w0 = pos >> 2, off = pos & 3;
+                                const int w1 = (w0 + 1) * 4 == z ? 0 : w0 + 1;  // wraps at z
+                                if (k < z)
+                                    pb[u] ^= __byte_perm(__ldcg(colw + w0), __ldcg(colw + w1), 0x3210 + 0x1111 * off);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < kCk; u++) {
+                        const uint32_t x = pb[u];
+                        const uint32_t lanes = (x | x >> 8 | x >> 16 | x >> 24) & 0xffu;
+                        const uint32_t nw = lanes & need & ~known;
+                        if (nw) {  // remember one failed check of the first new lane
+                            const int l = __ffs(nw) - 1;
+                            int i = 0;
+                            while (!((x >> (8 * i + l)) & 1)) i++;
+                            hint[l] = s * z + k0 + u * kThreads * 4 + i + 1;
+                        }
+                        acc |= lanes;
+                    }
+                    if (!QCL_FLOW_CHECK_EARLY) continue;
+                    const uint32_t wacc = __reduce_or_sync(0xffffffffu, acc);
+                    if ((ct & 31) == 0 && (wacc & need & ~known)) atomicOr(unsat, wacc);  // publish
+                    known |= wacc | __shfl_sync(0xffffffffu, kn, 0);  // warp-uniform
+                    if ((known & need) == need) {
+                        done = true;
+                        break;
+                    }
+                }
+                continue;
+            }
+            // any z: four checks per thread in flight, all d x 4 byte loads issued before the XORs
+            for (int kw = ct & ~31; kw < z; kw += kCk * kThreads) {  // warp-uniform trip count
+                const int k0 = kw + (ct & 31);
+                // the other check items of (g, t) publish what they find: re-read with the loads
+                const uint32_t kn = (ct & 31) == 0 ? __ldcg(unsat) : 0u;
+                uint32_t pb[kCk];
+#pragma unroll
+                for (int u = 0; u < kCk; u++) {
                     const int k = k0 + u * kThreads;
                     pb[u] = (a.synpack && k < z) ? __ldg(a.synpack + ((size_t)s * z + k) * a.G + g) : 0u;
                 }
@@ -535,7 +627,7 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
                         const uint8_t *colp = sg + (size_t)(ex & 0x7fff) * z;
                         const int sh = (int)(ex >> 16);
 #pragma unroll
-                        for (int u = 0; u < 4; u++) {
+                        for (int u = 0; u < kCk; u++) {
                             const int k = k0 + u * kThreads;
                             int pos = k + sh;
                             pos -= (pos >= z) ? z : 0;
@@ -543,8 +635,17 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
                         }
                     }
                 }
-                acc |= pb[0] | pb[1] | pb[2] | pb[3];
-                if (QCL_FLOW_CHECK_EARLY && ((__reduce_or_sync(0xffffffffu, acc) | known) & need) == need) {
+#pragma unroll
+                for (int u = 0; u < kCk; u++) {
+                    const uint32_t nw = pb[u] & need & ~known;
+                    if (nw) hint[__ffs(nw) - 1] = s * z + k0 + u * kThreads + 1;
+                    acc |= pb[u];
+                }
+                if (!QCL_FLOW_CHECK_EARLY) continue;
+                const uint32_t wacc = __reduce_or_sync(0xffffffffu, acc);
+                if ((ct & 31) == 0 && (wacc & need & ~known)) atomicOr(unsat, wacc);  // publish
+                known |= wacc | __shfl_sync(0xffffffffu, kn, 0);  // warp-uniform
+                if ((known & need) == need) {
                     done = true;
                     break;
                 }

@@ -163,7 +163,7 @@ struct qcl_state {
     int32_t f_check_items = 0;     // check items per lane group and sweep
     uint8_t *fsnap = nullptr;   // [2][G][n]
     uint8_t *fsign = nullptr;   // [G][n]
-    int *fet = nullptr;         // cdone | decided | unsat[2], each [G] x QCL_FLAG_STRIDE
+    int *fet = nullptr;         // cdone | decided | unsat[2] | hint, each [G] x QCL_FLAG_STRIDE
     uint32_t *famask = nullptr; // [G]
     // frame pool (qcl_state_decode_pool): per lane frame index / iterations, refill list
     bool pool_active = false;
@@ -606,7 +606,7 @@ static int ensure_flow_et(qcl_state *st) {
                        st->stream));
     CK(cudaMalloc(&st->fsnap, (size_t)2 * st->G * p->n));
     CK(cudaMalloc(&st->fsign, (size_t)st->G * p->n));
-    CK(cudaMalloc(&st->fet, sizeof(int) * 4 * QCL_FLAG_STRIDE * (size_t)st->G));
+    CK(cudaMalloc(&st->fet, sizeof(int) * 5 * QCL_FLAG_STRIDE * (size_t)st->G));
     CK(cudaMalloc(&st->famask, sizeof(uint32_t) * st->G));
     CK(cudaStreamSynchronize(st->stream));
     return QCL_OK;
@@ -1518,7 +1518,7 @@ static int enqueue_decode_fused_et(qcl_state *st, const qcl_config *cfg) {
         st->launches_all++;
     }
     if ((rc = enqueue_flow_reset(st, 1))) return rc;
-    CK(cudaMemsetAsync(st->fet, 0, sizeof(int) * 4 * QCL_FLAG_STRIDE * (size_t)st->G, st->stream));
+    CK(cudaMemsetAsync(st->fet, 0, sizeof(int) * 5 * QCL_FLAG_STRIDE * (size_t)st->G, st->stream));
     cudaEvent_t a = nullptr, b = nullptr;
     if (st->profiling) {
         CK(cudaEventCreate(&a));

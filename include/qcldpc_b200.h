@@ -157,7 +157,8 @@ int qcl_state_set_engine(qcl_state *st, int32_t engine);
 
 /* ---- asynchronous path (streaming / overlapped host<->device copies) ---------------
  * Everything below only enqueues work on the state's stream; qcl_state_wait blocks until
- * the results requested by qcl_state_results_async have landed.  Result buffers should
+ * all of it has completed (the results requested by qcl_state_results_async have landed;
+ * decode_ms: the last decode's device time, 0 if none was queued).  Result buffers should
  * be pinned (qcl_host_alloc) for the copies to overlap device work; pageable LLR inputs
  * are converted and staged through pinned chunks by host threads before the call returns
  * (the caller may reuse them at once), pinned ones are read asynchronously.

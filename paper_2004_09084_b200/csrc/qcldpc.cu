@@ -128,7 +128,7 @@ struct qcl_state {
     bool truths_valid = false;  // the last synthetic fill was encode mode (else all-zero words)
     void *staging = nullptr;
     size_t staging_bytes = 0;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_done = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     void *staging2 = nullptr;  // syndrome staging (async path: LLR staging may still be in flight)
     size_t staging2_bytes = 0;
     int engine = 4;  // flow engine where eligible, else the TMA per-layer kernels
@@ -1095,7 +1095,6 @@ int qcl_state_create(qcl_plan *p, int64_t batch, int32_t precision, qcl_state **
     for (int i = 0; i < 2 && e == cudaSuccess; i++) e = cudaEventCreateWithFlags(&st->ev_flag[i], cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreate(&st->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&st->ev1);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&st->ev_done, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMemsetAsync(st->llr, 0, nl * st->esz, st->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st->stream);
     if (e != cudaSuccess) {
@@ -1140,7 +1139,6 @@ int qcl_state_destroy(qcl_state *st) {
         if (st->ev_flag[i]) cudaEventDestroy(st->ev_flag[i]);
     if (st->ev0) cudaEventDestroy(st->ev0);
     if (st->ev1) cudaEventDestroy(st->ev1);
-    if (st->ev_done) cudaEventDestroy(st->ev_done);
     if (st->staging2) cudaFree(st->staging2);
     st->ring.release();
     if (st->stream) cudaStreamDestroy(st->stream);
@@ -1711,7 +1709,16 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
 static int finish_decode(qcl_state *st, float *elapsed_ms) {
     CK(cudaEventSynchronize(st->ev1));
     CK(cudaGetLastError());
-    if (elapsed_ms) CK(cudaEventElapsedTime(elapsed_ms, st->ev0, st->ev1));
+    if (elapsed_ms) {
+        // a wait with no decode recorded yet (only uploads or downloads queued): 0 ms
+        const cudaError_t e = cudaEventElapsedTime(elapsed_ms, st->ev0, st->ev1);
+        if (e == cudaErrorInvalidResourceHandle) {
+            cudaGetLastError();
+            *elapsed_ms = 0.0f;
+        } else {
+            CK(e);
+        }
+    }
     for (auto &ev : st->sweep_events) {
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, ev.first, ev.second));
@@ -1882,14 +1889,13 @@ int qcl_state_results_async(qcl_state *st, uint8_t *words, uint8_t *converged, i
     if (converged) CK(cudaMemcpyAsync(converged, st->conv, st->B, cudaMemcpyDeviceToHost, st->stream));
     if (iterations)
         CK(cudaMemcpyAsync(iterations, st->iters, st->B * sizeof(int64_t), cudaMemcpyDeviceToHost, st->stream));
-    CK(cudaEventRecord(st->ev_done, st->stream));
     return QCL_OK;
 }
 
 int qcl_state_wait(qcl_state *st, float *decode_ms) {
     if (!st) return fail(QCL_EVALUE, "NULL argument");
     DEVICE_SCOPE(st->plan->device);
-    CK(cudaEventSynchronize(st->ev_done));
+    CK(cudaStreamSynchronize(st->stream));  // everything queued on the state, results included
     return finish_decode(st, decode_ms);
 }
 

@@ -51,6 +51,21 @@ CODE = ROOT / "codes" / "standin_v2_z2500.txt"
 BYTES_PER_EDGE_ITER = {"fp32": 16, "fp64": 32, "fp32-msg16": 12}
 
 
+
+def single_codeword_l2(latency_ms):
+    """L2 traffic of one single-codeword decode from the committed ncu capture
+    (tools/single_codeword_profile.py -> profiles/r02_single_codeword_l2.json), over the
+    live latency: the decode is bound by its chain of dependent layer steps, not by L2."""
+    path = ROOT / "profiles" / "r02_single_codeword_l2.json"
+    if not path.exists():
+        return {}
+    prof = json.loads(path.read_text())
+    return {"l2_bytes_per_decode": prof["l2_bytes"], "l2_gbs": prof["l2_bytes"] / latency_ms / 1e6,
+            "l2_source": path.name, "layer_launches_profiled": prof["launches"],
+            "bound": "dependent layer steps (~3 us each, launch + L2 round trips), L2 throughput "
+                     f"{prof['time_weighted_pct_of_peak'].get('lts__t_sectors.avg.pct_of_peak_sustained_elapsed', 0):.1f}% "
+                     "of peak per launch under ncu"}
+
 def peaks():
     try:
         p = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -436,6 +451,7 @@ def run_b200(args):
             "update_launches_per_decode": int(b1_launches),
             "note": "device time (CUDA events) of qcl_state_decode with the LLRs resident; one-lane layout, "
                     "per-layer kernels in one CUDA graph with programmatic dependent launch",
+            **single_codeword_l2(float(np.median(b1_ms))),
         },
     }
     if shared:

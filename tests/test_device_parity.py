@@ -546,3 +546,18 @@ def test_stream_results_outlive_their_slots(gpu):
     dec = None
     gc.collect()
     assert np.array_equal(kept[0], snapshot)
+
+
+def test_wait_covers_uploads_without_a_decode(gpu):
+    """qcl_state_wait blocks for everything queued on the state (here only the staged LLR
+    upload) and reports 0 ms when no decode was queued (it used to fail on the unrecorded
+    timing events)."""
+    from paper_2004_09084_b200 import _native
+
+    base, sched, index = load_code("demo_4x8_z100")
+    n = base.n_cols * base.z
+    st = _native.State(_native.Plan(index, sched, 0), 4, "fp32")
+    llr = np.random.default_rng(5).normal(1.0, 2.0, size=(4, n))
+    st.set_llr(llr)
+    assert st.wait() == 0.0
+    assert np.array_equal(st.get_llr(), llr.astype(np.float32).astype(np.float64))

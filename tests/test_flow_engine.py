@@ -215,3 +215,40 @@ def test_one_decoder_shared_by_threads(gpu):
             for w, g in zip(want, got):
                 for a, b in zip(w, g):
                     assert np.array_equal(a, b), (precision, et)
+
+
+@pytest.mark.parametrize("z", [37, 40, 101, 128])
+def test_fused_et_converging_frames_nonzero_targets(gpu, z):
+    """Fused early termination where frames converge at different sweeps toward nonzero
+    targets (s = H x for a random word x, LLRs pointing at x with noise): the check items'
+    word-wise scan (z % 4 == 0) and byte scan (z odd), the last-failed-check hints and the
+    shared early exit all feed the decisions; outcomes equal the per-layer engine's bit for
+    bit and every converged word satisfies its target."""
+    import paper_2004_09084_b200 as q
+    from conftest import make_code
+
+    rng = np.random.default_rng(z)
+    n_rows, n_cols = 6, 16
+    shifts = np.full((n_rows, n_cols), -1, dtype=np.int64)
+    for i in range(n_rows):
+        cols = rng.choice(n_cols, size=int(rng.integers(3, 9)), replace=False)
+        shifts[i, cols] = rng.integers(0, z, size=len(cols))
+    base, sched, index = make_code(shifts.tolist(), z, merged=True)
+    n, m = n_cols * z, n_rows * z
+    B = 72
+    x = (rng.random((B, n)) < 0.5).astype(np.uint8)
+    rows = q.expand(base)
+    syn = np.stack([x[:, r].sum(axis=1) & 1 for r in rows], axis=1).astype(np.uint8)
+    # per-frame noise level: some frames converge in a sweep or two, others late or never
+    sigma = rng.uniform(0.5, 1.1, size=(B, 1))
+    llr = (1.0 - 2.0 * x) * 2.0 / sigma**2 + rng.normal(0.0, 1.0, size=(B, n)) * 2.0 / sigma
+    cfg = q.DecoderConfig(max_iterations=30, early_termination=True)
+    want = q.LayeredDecoder(index, sched, cfg, precision="fp32", engine=0).decode_batch_arrays(llr, syn)
+    got = q.LayeredDecoder(index, sched, cfg, precision="fp32", engine=4).decode_batch_arrays(llr, syn)
+    for a, b in zip(want, got):
+        assert np.array_equal(a, b)
+    w, c, it = got
+    print(f"z={z}: {int(c.sum())}/{B} converged, iterations {np.bincount(it).nonzero()[0].tolist()}")
+    assert 5 < c.sum() < B - 5 and len(set(it[c].tolist())) >= 3  # a spread of convergence sweeps
+    got_syn = np.stack([w[:, r].sum(axis=1) & 1 for r in rows], axis=1).astype(np.uint8)
+    assert np.array_equal(got_syn[c], syn[c])

@@ -232,6 +232,9 @@ inline void flow_sweep_divisor(uint32_t d, uint32_t &mul, uint32_t &shift) {
 //   1: ld.acquire.gpu on every flag load (a PTX-model synchronizes-with edge): +4.8% per
 //      decode in bursts, +5.8% sustained (tools/flow_sustained.py, DESIGN 3.1);
 //   2: relaxed polls, then one fence.acq_rel.gpu per resolved tile: +12%.
+#ifndef QCL_FLOW_STATIC
+#define QCL_FLOW_STATIC 0
+#endif
 #ifndef QCL_FLOW_ACQUIRE
 #define QCL_FLOW_ACQUIRE 0
 #endif
@@ -992,15 +995,25 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         // through a small queue, so dependency polling overlaps the bulk-copy issue.
         const int t_base = a.t_dev ? *(volatile const int *)a.t_dev : a.t_base;
         int n2 = 0;
-        if (lane == 0) n2 = atomicAdd(a.counter, 1);
         // stop: every frame converged (fused ET) -- the items already claimed (the one in
         // hand and the prefetched one) are still processed, nothing new is claimed
         bool stop = false;
+#if QCL_FLOW_STATIC
+        // static round-robin items (probe: needs every CTA co-resident)
+        n2 = blockIdx.x;
+        auto next_claim = [&]() {
+            const int n = n2;
+            if (n < a.item_end) n2 = stop ? a.item_end : n + (int)gridDim.x;
+            return n;
+        };
+#else
+        if (lane == 0) n2 = atomicAdd(a.counter, 1);
         auto next_claim = [&]() {
             const int n = __shfl_sync(0xffffffffu, n2, 0);
             if (n < a.item_end && lane == 0) n2 = stop ? a.item_end : atomicAdd(a.counter, 1);
             return n;
         };
+#endif
         auto record = [&](int n) {
             int t;
             return __ldg(a.items + flow_item_map(a, n, t));

@@ -196,8 +196,8 @@ struct Item {
     bool live;
 };
 template <int V>
-__device__ __forceinline__ Item map_item(const SlotRange &r) {
-    int blk = blockIdx.x;
+__device__ __forceinline__ Item map_item(const SlotRange &r, int blk = -1) {
+    if (blk < 0) blk = blockIdx.x;
     const int chunk = blk % r.bps;
     blk /= r.bps;
     Item it;
@@ -452,6 +452,10 @@ __device__ __forceinline__ void check_update(double (&q)[D][V], double (&ph)[D][
 // columns (checked at plan creation, decoder.py:144-154), so the read-modify-write of
 // L is race free.  Offsets inside a lane group are 32-bit (n*W and E*z*W < 2^31).
 template <typename T, int V, int DMAX, bool HAS_SYN>
+__device__ __forceinline__ void layer_tile(const LayerArgs &a, const Item &it, const SlotInfo &si,
+                                           const EdgeInfo *s_edge);
+
+template <typename T, int V, int DMAX, bool HAS_SYN>
 __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
     // programmatic dependent launch (qcldpc.cu launch_pdl): the next layer's grid may start
     // now; this one's prologue (immutable plan tables) overlaps the previous layer's tail,
@@ -466,7 +470,15 @@ __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
     if (a.n_active && *(volatile const int *)a.n_active == 0) return;
     __syncthreads();
     if (!it.live) return;
+    layer_tile<T, V, DMAX, HAS_SYN>(a, it, si, s_edge);
+}
 
+// The update of one thread's check(s) (decoder.py:212-250): shared by the per-layer
+// kernel above and the persistent single-launch kernel below.
+template <typename T, int V, int DMAX, bool HAS_SYN>
+__device__ __forceinline__ void layer_tile(const LayerArgs &a, const Item &it, const SlotInfo &si,
+                                           const EdgeInfo *s_edge) {
+    const int d = si.degree;
     const int z = a.r.z, lw = a.r.lw, k = it.k;
     T *Lg = reinterpret_cast<T *>(a.L) + (((size_t)it.g * a.r.n) << lw) + it.w0;
     T *Rg = reinterpret_cast<T *>(a.R) + (((((size_t)it.g * a.r.E + si.edge_off) * z) + k) << lw) + it.w0;
@@ -507,6 +519,142 @@ __global__ void __launch_bounds__(kBlock) layer_kernel(LayerArgs a) {
         if (j < d) {
             vstore<T, V>(Rg + ((uint32_t)(j * z) << lw), ph[j]);
             vstore<T, V>(Lg + loff[j], q[j]);
+        }
+    }
+}
+
+// ---- persistent per-layer engine for one or two codewords (BASELINE configs[1]) -------
+// With W <= 2 lanes every layer is a few hundred CTAs of dependent work, and a decode is
+// ~1650 dependent layer launches whose launch gaps set the latency (PDL hides part of
+// it).  Here the whole decode is ONE cooperative launch: every CTA walks the launch units
+// of a sweep in schedule order (decoder.py:259-262), takes the blocks b = blockIdx.x,
+// blockIdx.x + gridDim.x, ... of each unit (the same check-to-thread map and the same
+// layer_tile arithmetic as layer_kernel, so results are bit-identical to it), and a
+// grid barrier separates consecutive units (layer l + 1 reads what layer l wrote).
+struct alignas(16) PersistUnit {
+    LayerArgs a;
+    int32_t blocks;  // G * nslots * bps
+    int32_t dcls;    // DMAX bucket of the unit: 4, 8, 12, 16 or 32
+    int32_t layer;   // merged layer (units of one layer touch disjoint columns: no barrier)
+};
+struct PersistArgs {
+    const PersistUnit *units;  // [nu] one sweep, schedule order
+    int32_t nu, sweeps;
+    int32_t S, E, nlist;       // plan tables copied to shared memory at kernel start
+    const SlotInfo *slots;
+    const EdgeInfo *edges;
+    const int32_t *slot_list;
+    unsigned *bar;             // [0] completed barriers, [32] arrivals, [32 (5 + cta)] per-CTA arrivals
+                               // (zeroed before the launch)
+    const int *n_active;       // early termination: skip the launch once every frame converged
+    int32_t bar_mode;          // persist_grid_barrier
+};
+static_assert(sizeof(PersistUnit) % 16 == 0, "PersistUnit is copied in 16-byte words");
+__host__ __device__ constexpr size_t persist_smem_bytes(int nu, int S, int E, int nlist) {
+    return sizeof(PersistUnit) * nu + sizeof(SlotInfo) * S + sizeof(EdgeInfo) * E + sizeof(int32_t) * nlist;
+}
+
+// Barrier k of the launch (bar.sync orders each CTA's global stores before its thread-0
+// release -- cumulativity -- and the acquire polls order the next unit's loads after every
+// CTA's stores).  Modes (PersistArgs::bar_mode, QCL_PERSIST_BAR):
+//   0: one acq_rel atomic arrival per CTA; the CTA whose arrival completes the count
+//      releases the barrier word (a separate line) that the others poll;
+//   1: fire-and-forget release reductions, every CTA polls the arrival counter;
+//   2: per-CTA arrival flags (one line each) gathered by CTA 0, which releases the word.
+// Single codeword, 50 iterations (tools/persist_sweep.sh): 1 = 4.44 ms, 0 = 5.31, 2 = 6.10;
+// a 32 ns poll back-off (4.53) and arrivals spread over four lines (5.82) were slower.
+constexpr int kPersistThreads = 512;  // at most two 256-check blocks per CTA
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void persist_grid_barrier(unsigned *bar, unsigned k, int mode) {
+    __syncthreads();
+    if (mode == 2) {
+        if (threadIdx.x == 0) st_release_u32(bar + 32 * (5 + blockIdx.x), k);
+        if (blockIdx.x == 0) {
+            for (int c = threadIdx.x; c < (int)gridDim.x; c += blockDim.x)
+                while (ld_acquire_u32(bar + 32 * (5 + c)) < k) {
+                }
+            __syncthreads();
+            if (threadIdx.x == 0) st_release_u32(bar, k);
+        } else if (threadIdx.x == 0) {
+            while (ld_acquire_u32(bar) < k) {
+            }
+        }
+    } else if (threadIdx.x == 0) {
+        if (mode == 1) {
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 32) : "memory");
+            while (ld_acquire_u32(bar + 32) < k * gridDim.x) {
+            }
+        } else {
+            unsigned old;
+            asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar + 32) : "memory");
+            if (old == k * gridDim.x - 1)
+                st_release_u32(bar, k);
+            else
+                while (ld_acquire_u32(bar) < k) {
+                }
+        }
+    }
+    __syncthreads();
+}
+
+template <typename T, bool HAS_SYN, int MAXD>  // MAXD: the largest unit bucket of the plan
+__global__ void __launch_bounds__(kPersistThreads, 1) layer_persist_kernel(PersistArgs pa) {
+    extern __shared__ __align__(16) unsigned char psm[];
+    PersistUnit *units = reinterpret_cast<PersistUnit *>(psm);
+    SlotInfo *slots = reinterpret_cast<SlotInfo *>(units + pa.nu);
+    EdgeInfo *edges = reinterpret_cast<EdgeInfo *>(slots + pa.S);
+    int32_t *slist = reinterpret_cast<int32_t *>(edges + pa.E);
+    if (pa.n_active && *(volatile const int *)pa.n_active == 0) return;  // uniform: set between launches
+    {
+        const int4 *src = reinterpret_cast<const int4 *>(pa.units);
+        int4 *dst = reinterpret_cast<int4 *>(units);
+        for (int i = threadIdx.x; i < (int)(sizeof(PersistUnit) / 16) * pa.nu; i += blockDim.x) dst[i] = src[i];
+        for (int i = threadIdx.x; i < pa.S; i += blockDim.x) slots[i] = pa.slots[i];
+        for (int i = threadIdx.x; i < pa.E; i += blockDim.x) edges[i] = pa.edges[i];
+        for (int i = threadIdx.x; i < pa.nlist; i += blockDim.x) slist[i] = pa.slot_list[i];
+    }
+    __syncthreads();
+    unsigned k = 0;
+    for (int t = 0; t < pa.sweeps; t++) {
+        for (int u = 0; u < pa.nu; u++) {
+            const PersistUnit &pu = units[u];
+            const SlotRange &r = pu.a.r;
+            const int nb = pu.blocks, dc = pu.dcls;
+            const int halves = blockDim.x / kBlock;
+            const int tid = threadIdx.x % kBlock;
+            for (int b = blockIdx.x * halves + threadIdx.x / kBlock; b < nb; b += gridDim.x * halves) {
+                // map_item<1> with the slot list in shared memory
+                const int chunk = b % r.bps, blk = b / r.bps;
+                Item it;
+                it.slot = slist[r.slot0 + blk % r.nslots];
+                it.g = r.g0 + blk / r.nslots;
+                const int item = chunk * kBlock + tid;
+                it.live = item < (r.z << r.lw);
+                it.k = item >> r.lw;
+                it.w0 = item - (it.k << r.lw);
+                if (!it.live) continue;
+                const SlotInfo si = slots[it.slot];
+                const EdgeInfo *se = edges + si.edge_off;
+                if (dc == 4)
+                    layer_tile<T, 1, 4, HAS_SYN>(pu.a, it, si, se);
+                else if (MAXD >= 8 && dc == 8)
+                    layer_tile<T, 1, (MAXD >= 8 ? 8 : 4), HAS_SYN>(pu.a, it, si, se);
+                else if (MAXD >= 12 && dc == 12)
+                    layer_tile<T, 1, (MAXD >= 12 ? 12 : 4), HAS_SYN>(pu.a, it, si, se);
+                else if (MAXD >= 16 && dc == 16)
+                    layer_tile<T, 1, (MAXD >= 16 ? 16 : 4), HAS_SYN>(pu.a, it, si, se);
+                else if (MAXD >= 32)
+                    layer_tile<T, 1, (MAXD >= 32 ? 32 : 4), HAS_SYN>(pu.a, it, si, se);
+            }
+            if (u + 1 < pa.nu && units[u + 1].layer == pu.layer) continue;  // same layer: disjoint columns
+            persist_grid_barrier(pa.bar, ++k, pa.bar_mode);
         }
     }
 }

@@ -174,6 +174,13 @@ struct qcl_state {
     int32_t *prefill = nullptr;    // [Bp] lanes to refill this sweep
     int32_t *pcount = nullptr;     // [0] refills this sweep, [1] frames handed out
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> sweep_events;
+    // persistent per-layer engine (W <= 2 lanes): unit table of one sweep, barrier counter
+    PersistUnit *punits = nullptr;
+    unsigned *pbar = nullptr;
+    int p_nu = 0, p_grid = 0, p_maxd = 4;
+    double p_clip = -1, p_eps = -1;
+    bool p_syn = false;
+    bool persist_decode = false;  // this decode runs on the persistent per-layer engine
     HostRing ring;  // pinned chunks of the pageable-memory copy pipelines (hostio.h)
 };
 
@@ -468,6 +475,145 @@ static void enqueue_sweep(qcl_state *st, double clip, double eps) {
         cudaEventRecord(st->join[c - 1], st->side[c - 1]);
         cudaStreamWaitEvent(st->stream, st->join[c - 1], 0);
     }
+}
+
+// ------------------------------------------------- persistent per-layer engine (W <= 2)
+// One or two codewords (BASELINE configs[1]) run on the direct per-layer kernels, ~33
+// dependent launches per sweep.  layer_persist_kernel (kernels.cuh) runs every sweep of
+// the decode in ONE cooperative launch with a grid barrier between launch units; the
+// per-thread arithmetic is layer_tile, shared with layer_kernel, so the result is
+// bit-identical.  QCL_PERSIST=0 selects the per-layer launches.
+static size_t persist_smem(const qcl_state *st);
+static bool use_persist(const qcl_state *st) {
+    static const int on = env_int("QCL_PERSIST", 1);
+    // engines 0 / 4 where the lane rows are too narrow for bulk copies (engine 1 keeps
+    // the per-layer launches)
+    return on && (st->engine == 0 || st->engine == 4) && st->W <= 2 && !use_tma(st) && !st->msg16 &&
+           persist_smem(st) <= 160 * 1024;
+}
+
+template <typename T, bool SYN>
+static void (*persist_kernel(int maxd))(PersistArgs) {
+    switch (maxd) {
+        case 4: return layer_persist_kernel<T, SYN, 4>;
+        case 8: return layer_persist_kernel<T, SYN, 8>;
+        case 12: return layer_persist_kernel<T, SYN, 12>;
+        case 16: return layer_persist_kernel<T, SYN, 16>;
+        default: return layer_persist_kernel<T, SYN, 32>;
+    }
+}
+static void (*persist_kernel(const qcl_state *st))(PersistArgs) {
+    if (st->prec == QCL_PREC_FP32)
+        return st->has_syn ? persist_kernel<float, true>(st->p_maxd) : persist_kernel<float, false>(st->p_maxd);
+    return st->has_syn ? persist_kernel<double, true>(st->p_maxd) : persist_kernel<double, false>(st->p_maxd);
+}
+
+constexpr size_t kPersistBarBytes = 128 * (5 + 1024);  // barrier word, arrivals, one line per CTA (<= 1024)
+static int persist_threads() {
+    static const int t = env_int("QCL_PERSIST_THREADS", 256) == 512 ? 512 : 256;
+    return t;
+}
+static size_t persist_smem(const qcl_state *st) {
+    const qcl_plan *p = st->plan;
+    return persist_smem_bytes((int)p->units.size(), p->S, p->E, (int)p->h_slot_list.size());
+}
+
+static int persist_grid(const qcl_state *st, int max_blocks) {
+    int sms = 0, per_sm = 0;
+    const size_t smem = persist_smem(st);
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, st->plan->device));
+    CK(cudaFuncSetAttribute(persist_kernel(st), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist_kernel(st), persist_threads(), smem));
+    if (per_sm < 1) return 0;
+    // one CTA per SM and lane (tools/persist_sweep.sh: B = 1 4.52 ms at one CTA per SM
+    // against 4.66 at two; B = 2 4.95 against 5.50)
+    static const int cap = env_int("QCL_PERSIST_CTAS_PER_SM", 0);
+    per_sm = std::min(per_sm, cap > 0 ? cap : st->W);
+    const int halves = persist_threads() / kBlock;
+    return std::max(1, std::min({(max_blocks + halves - 1) / halves, sms * per_sm, 1024}));
+}
+
+// Unit table of one sweep for (clip, eps, syndrome presence); uploaded outside any graph
+// capture on the state's stream and waited for there.
+static int ensure_persist(qcl_state *st, double clip, double eps) {
+    if (st->punits && st->p_clip == clip && st->p_eps == eps && st->p_syn == st->has_syn) return QCL_OK;
+    const qcl_plan *p = st->plan;
+    std::vector<PersistUnit> units;
+    int max_blocks = 1, maxd = 4;
+    for (const auto &u : p->units) {
+        PersistUnit pu{};
+        LayerArgs &a = pu.a;
+        a.r = slot_range(st, u.list_off, u.count, 1, p->slot_list);
+        a.r.g0 = 0;
+        a.L = st->L;
+        a.R = st->R;
+        a.syn = st->has_syn ? st->syn : nullptr;
+        a.uniform = p->layer_uniform[u.layer];
+        a.clip_r = clip <= 1.001 * log1p(2.0 / expm1(eps));
+        a.n_active = nullptr;
+        a.clip = clip;
+        a.eps = eps;
+        a.mag_max = mag_bound(clip, eps);
+        pu.blocks = (int32_t)((int64_t)st->G * a.r.nslots * a.r.bps);
+        pu.dcls = dmax_bucket(u.dmax);
+        pu.layer = u.layer;
+        maxd = std::max(maxd, pu.dcls);
+        max_blocks = std::max(max_blocks, pu.blocks);
+        units.push_back(pu);
+    }
+    CK(cudaStreamSynchronize(st->stream));  // a previous decode may still read the old table
+    if (!st->punits || st->p_nu < (int)units.size()) {
+        if (st->punits) cudaFree(st->punits);
+        st->punits = nullptr;
+        CK(cudaMalloc(&st->punits, sizeof(PersistUnit) * units.size()));
+    }
+    if (!st->pbar) CK(cudaMalloc(&st->pbar, kPersistBarBytes));
+    CK(cudaMemcpyAsync(st->punits, units.data(), sizeof(PersistUnit) * units.size(), cudaMemcpyHostToDevice,
+                       st->stream));
+    CK(cudaStreamSynchronize(st->stream));
+    st->p_nu = (int)units.size();
+    st->p_maxd = maxd;
+    st->p_grid = persist_grid(st, max_blocks);
+    if (st->p_grid <= 0) return fail(QCL_ECUDA, "persistent engine: no occupancy");
+    st->p_clip = clip;
+    st->p_eps = eps;
+    st->p_syn = st->has_syn;
+    return QCL_OK;
+}
+
+// `sweeps` sweeps in one cooperative launch (all CTAs co-resident: the grid barrier
+// cannot deadlock, also next to other work on the device).
+static int enqueue_persist(qcl_state *st, int sweeps, bool et) {
+    const qcl_plan *p = st->plan;
+    CK(cudaMemsetAsync(st->pbar, 0, kPersistBarBytes, st->stream));
+    PersistArgs pa;
+    pa.units = st->punits;
+    pa.nu = st->p_nu;
+    pa.S = p->S;
+    pa.E = p->E;
+    pa.nlist = (int)p->h_slot_list.size();
+    pa.slots = p->slots;
+    pa.edges = p->edges;
+    pa.slot_list = p->slot_list;
+    pa.sweeps = sweeps;
+    pa.bar = st->pbar;
+    pa.n_active = et ? st->n_active : nullptr;
+    static const int bar_mode = env_int("QCL_PERSIST_BAR", 1);  // 1 measured best (DESIGN 3.4)
+    pa.bar_mode = bar_mode;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)st->p_grid);
+    cfg.blockDim = dim3(persist_threads());
+    cfg.dynamicSmemBytes = persist_smem(st);
+    cfg.stream = st->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, persist_kernel(st), pa));
+    st->launches_layer++;
+    st->launches_all++;
+    return QCL_OK;
 }
 
 // ------------------------------------------------------------ flow engine (engine 4)
@@ -1131,7 +1277,7 @@ int qcl_state_destroy(qcl_state *st) {
                       (void *)st->prefill, (void *)st->pcount,
                       (void *)st->fitems, (void *)st->fflags, (void *)st->fcounters, (void *)st->fstats,
                       (void *)st->fitems_et, (void *)st->fsnap, (void *)st->fsign, (void *)st->fet,
-                      (void *)st->famask})
+                      (void *)st->famask, (void *)st->punits, (void *)st->pbar})
         if (ptr) cudaFree(ptr);
     if (st->h_n_active) cudaFreeHost(st->h_n_active);
     if (st->h_flag) cudaFreeHost(st->h_flag);
@@ -1552,7 +1698,11 @@ static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
     enqueue_group_active(st);
     st->g_et = et;
     const bool flow = st->flow_decode;
+    const bool persist = st->persist_decode;
     if ((rc = enqueue_reset(st, cfg->llr_clip, !flow))) return rc;  // flow: sweep 0 zeroes r_old itself
+    if (persist && !et) {  // every sweep in one cooperative launch
+        if ((rc = enqueue_persist(st, cfg->max_iterations, false))) return rc;
+    }
     if (flow) {
         if ((rc = enqueue_flow_reset(st, et ? cfg->max_iterations : 1))) return rc;
         if (!et) {  // every sweep in one persistent launch, degree-1 edges deferred
@@ -1562,9 +1712,12 @@ static int enqueue_decode_body(qcl_state *st, const qcl_config *cfg) {
         }
     }
     for (int t = 1; t <= cfg->max_iterations; t++) {
-        if (flow && !et) break;
+        if ((flow || persist) && !et) break;
         const int64_t before = st->launches_layer;
-        if (flow) {
+        if (persist) {
+            if ((rc = enqueue_persist(st, 1, true))) return rc;
+            st->launches_all -= st->launches_layer - before;  // counted below
+        } else if (flow) {
             if ((rc = enqueue_flow(st, cfg->llr_clip, cfg->phi_epsilon, t - 1, 1, t - 1, true, -1, nullptr, 0)))
                 return rc;
             st->launches_all -= st->launches_layer - before;  // counted below
@@ -1613,6 +1766,8 @@ static int enqueue_decode(qcl_state *st, const qcl_config *cfg, bool sync) {
         fused = (int64_t)cfg->max_iterations * st->f_sweep_items_et * st->f_nblk + 8LL * st->f_grid < (1LL << 31);
     }
     st->fused_et = fused;
+    st->persist_decode = !st->flow_decode && use_persist(st);
+    if (st->persist_decode && (rc = ensure_persist(st, cfg->llr_clip, cfg->phi_epsilon))) return rc;
     if (fused && st->profiling) {
         CK(cudaEventRecord(st->ev0, st->stream));
         if ((rc = enqueue_decode_fused_et(st, cfg))) return rc;

@@ -232,9 +232,17 @@ inline void flow_sweep_divisor(uint32_t d, uint32_t &mul, uint32_t &shift) {
 //   1: ld.acquire.gpu on every flag load (a PTX-model synchronizes-with edge): +4.8% per
 //      decode in bursts, +5.8% sustained (tools/flow_sustained.py, DESIGN 3.1);
 //   2: relaxed polls, then one fence.acq_rel.gpu per resolved tile: +12%.
+// QCL_FLOW_STATIC: item assignment.  0: dynamic claims (atomicAdd) everywhere; 1: static
+// round-robin everywhere; 2 (default): static for the fused-ET kernel only.  Static
+// kernels are launched cooperatively (co-residency is then guaranteed, which the static
+// order needs for deadlock freedom).  No-ET decode: no difference (23.32 vs 23.34 ms
+// sustained); fused-ET sweep 0.516 -> 0.493 ms (profiles/r02_ab_static.log).
 #ifndef QCL_FLOW_STATIC
-#define QCL_FLOW_STATIC 0
+#define QCL_FLOW_STATIC 2
 #endif
+__host__ __device__ constexpr bool flow_static(bool etf) {
+    return QCL_FLOW_STATIC == 1 || (QCL_FLOW_STATIC == 2 && etf);
+}
 #ifndef QCL_FLOW_ACQUIRE
 #define QCL_FLOW_ACQUIRE 0
 #endif
@@ -278,10 +286,17 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 //   hence the #error above for other architectures.  Measured cost of the formal
 //   variant: +4.8% in bursts, +5.8% sustained; checked by tools/flow_stress.py (repeated
 //   decodes bit-identical to the per-layer engine) and the bit-exact engine tests.
-__device__ __forceinline__ int spin_until(const int *flag, int need) {
+// abort (fused ET with static items): stop waiting once every frame has converged -- the
+// tile waited for may belong to a CTA that has stopped; returns kSpinAborted then
+constexpr int kSpinAborted = -(1 << 24);
+__device__ __forceinline__ bool all_converged(const int *n_active) {
+    return n_active && *(volatile const int *)n_active == 0;
+}
+__device__ __forceinline__ int spin_until(const int *flag, int need, const int *abort = nullptr) {
     if (ld_flag(flag) >= need) return 0;
     int polls = 1;
     while (ld_flag(flag) < need) {
+        if (all_converged(abort)) return kSpinAborted;
         __nanosleep(64);
         polls++;
     }
@@ -293,8 +308,21 @@ __device__ __forceinline__ int ld_acquire_gpu(const int *p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void spin_until_acquire(const int *flag, int need) {
-    while (ld_acquire_gpu(flag) < need) __nanosleep(128);
+__device__ __forceinline__ bool spin_until_acquire(const int *flag, int need, const int *abort = nullptr) {
+    while (ld_acquire_gpu(flag) < need) {
+        if (all_converged(abort)) return false;
+        __nanosleep(128);
+    }
+    return true;
+}
+__device__ __forceinline__ bool consumers_sync_or(bool p) {  // consumers_sync + OR of p
+    uint32_t r;
+    asm volatile(
+        "{ .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.or.pred q, 1, %2, p;\n selp.u32 %0, 1, 0, q; }"
+        : "=r"(r)
+        : "r"((uint32_t)p), "n"(kFlowConsumers * 32)
+        : "memory");
+    return r != 0;
 }
 __device__ __forceinline__ void red_release_max(int *p, int v) {
     asm volatile("red.release.gpu.global.max.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -477,7 +505,8 @@ __device__ __forceinline__ void flow_snap(const FlowArgs &a, const FlowHdr &h, u
 // A check item (g, slots [h.slot, h.kt), sweep h.t), run by all consumer threads of the
 // CTA; sc: 3 words of shared scratch.  See "Fused early termination" above.
 __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, int ct, const uint2 *stab,
-                                           const uint2 *etab, uint32_t *sc) {
+                                           const uint2 *etab, uint32_t *sc, bool abort_waits) {
+    bool aborted = false;
     constexpr int kThreads = kFlowConsumers * 32;
     constexpr int kCk = 4;  // checks per thread in flight in a scan
     const int g = h.g, t = h.t, par = t & 1, z = a.z;
@@ -498,7 +527,7 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
         // flags of the group >= t + 1 (acquire; the barrier passes it to every thread)
         // relaxed polls, 8 in flight per thread, then one acquire fence per thread
         const int *fl = a.flags + (size_t)g * a.nkb_total * QCL_FLAG_STRIDE;
-        for (int i0 = ct; i0 < a.nkb_total; i0 += 8 * kThreads) {
+        for (int i0 = ct; i0 < a.nkb_total && !aborted; i0 += 8 * kThreads) {
             for (;;) {
                 int v[8];
 #pragma unroll
@@ -510,12 +539,21 @@ __device__ __forceinline__ void flow_check(const FlowArgs &a, const FlowHdr &h, 
 #pragma unroll
                 for (int u = 0; u < 8; u++) ok &= v[u] >= t + 1;
                 if (ok) break;
+                if (abort_waits && all_converged(a.n_active)) {
+                    aborted = true;
+                    break;
+                }
                 __nanosleep(128);
             }
         }
         asm volatile("fence.acq_rel.gpu;" ::: "memory");
     }
-    consumers_sync();  // uniform: every consumer thread computed the same `scan`
+    // uniform: every consumer thread computed the same `scan`
+    if (abort_waits) {
+        if (consumers_sync_or(aborted)) return;  // every frame converged: nothing left to decide
+    } else {
+        consumers_sync();
+    }
     const uint8_t *sg = a.snap + ((size_t)par * a.G + g) * a.n;
     // parity bits (lanes) of check k of slot s in this sweep's snapshot (^ target syndrome)
     auto check_bits = [&](int s, int k) {
@@ -998,22 +1036,22 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         // stop: every frame converged (fused ET) -- the items already claimed (the one in
         // hand and the prefetched one) are still processed, nothing new is claimed
         bool stop = false;
-#if QCL_FLOW_STATIC
-        // static round-robin items (probe: needs every CTA co-resident)
-        n2 = blockIdx.x;
+        // static round-robin items (flow_static<ETF>: launched cooperatively, so every
+        // CTA is co-resident and a CTA's items wait only on earlier items of running CTAs)
+        constexpr bool kStatic = flow_static(ETF);
+        if (kStatic) n2 = blockIdx.x;
+        else if (lane == 0) n2 = atomicAdd(a.counter, 1);
         auto next_claim = [&]() {
-            const int n = n2;
-            if (n < a.item_end) n2 = stop ? a.item_end : n + (int)gridDim.x;
-            return n;
+            if constexpr (kStatic) {
+                const int n = n2;
+                if (n < a.item_end) n2 = stop ? a.item_end : n + (int)gridDim.x;
+                return n;
+            } else {
+                const int n = __shfl_sync(0xffffffffu, n2, 0);
+                if (n < a.item_end && lane == 0) n2 = stop ? a.item_end : atomicAdd(a.counter, 1);
+                return n;
+            }
         };
-#else
-        if (lane == 0) n2 = atomicAdd(a.counter, 1);
-        auto next_claim = [&]() {
-            const int n = __shfl_sync(0xffffffffu, n2, 0);
-            if (n < a.item_end && lane == 0) n2 = stop ? a.item_end : atomicAdd(a.counter, 1);
-            return n;
-        };
-#endif
         auto record = [&](int n) {
             int t;
             return __ldg(a.items + flow_item_map(a, n, t));
@@ -1107,9 +1145,13 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                 // wait for the previous writers of every column of this tile: all covering
                 // flags of an edge are loaded together (one round trip), only stale ones polled
                 int polls = 0;
+                // static items: a wait may point at a tile whose CTA stopped after every frame
+                // converged -- abort it then (nothing observable is left to compute)
+                const int *abort = (kStatic && ETF && QCL_FLOW_ET_STOP) ? a.n_active : nullptr;
                 if (h.k0 < 0) {
                     // check item (g, slot, t): every tile of (g, t) stored, decisions in order
-                    if (lane == 0 && h.t >= 1) spin_until_acquire(a.decided + (size_t)h.g * QCL_FLAG_STRIDE, h.t);
+                    if (lane == 0 && h.t >= 1 && !spin_until_acquire(a.decided + (size_t)h.g * QCL_FLAG_STRIDE, h.t, abort))
+                        polls = kSpinAborted;
                     __syncwarp();
                 } else {
                     if (ETF && (slt[h.slot] >> 16) && h.t >= 2) {  // snapshot parity reuse
@@ -1117,7 +1159,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                         const bool cached = __shfl_sync(0xffffffffu, dec_tag == h.g && dec_val >= h.t - 1, owner);
                         if (!cached && lane == owner) {
                             const int *dp = a.decided + (size_t)h.g * QCL_FLAG_STRIDE;
-                            polls += spin_until(dp, h.t - 1);
+                            polls += spin_until(dp, h.t - 1, abort);
                             dec_tag = h.g;
                             dec_val = h.t - 1;
                         }
@@ -1130,8 +1172,12 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
                         if (m < nfl) fv[m] = ld_flag(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE);
 #pragma unroll
                     for (int m = 0; m < 4; m++)
-                        if (m < nfl && fv[m] < need) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need);
-                    for (int m = 4; m < nfl; m++) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need);
+                        if (m < nfl && fv[m] < need) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need, abort);
+                    for (int m = 4; m < nfl; m++) polls += spin_until(fl + (m < nlo ? lo + m : m - nlo) * QCL_FLAG_STRIDE, need, abort);
+                }
+                if (abort && __any_sync(0xffffffffu, polls < 0)) {
+                    stop = true;  // every frame converged: this item and the rest are dropped
+                    goto next_item;
                 }
                 flow_acquire_fence();
                 FLOW_TICK(2);
@@ -1281,7 +1327,7 @@ __global__ void __launch_bounds__(kFlowThreads, kFlowCtasPerSm) flow_kernel(Flow
         } else {
             float *stage = stages + (size_t)s * kStageElems;
             if (ETF && h.k0 < 0) {
-                if constexpr (ETF) flow_check(a, h, ct, stab, etab, scratch);
+                if constexpr (ETF) flow_check(a, h, ct, stab, etab, scratch, flow_static(ETF) && QCL_FLOW_ET_STOP);
             } else if (h.cls == 0) {
                 flow_consume<flow_class_V(0), 4, HAS_SYN, RT, ETF>(a, h, stage, ct, etab, slt[h.slot]);
             } else if (h.cls == 1) {

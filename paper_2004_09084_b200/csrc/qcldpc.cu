@@ -844,7 +844,21 @@ static int enqueue_flow(qcl_state *st, double clip, double eps, int t0, int T, i
     else
         kern = st->has_syn ? (prof ? flow_kernel<true, true> : flow_kernel<true, false>)
                            : (prof ? flow_kernel<false, true> : flow_kernel<false, false>);
-    kern<<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
+    if (flow_static(etf)) {  // static item order: all CTAs must be co-resident
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(kFlowThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        CK(cudaLaunchKernelEx(&cfg, kern, a));
+    } else {
+        kern<<<(unsigned)grid, kFlowThreads, smem, st->stream>>>(a);
+    }
     CK(cudaGetLastError());
     st->launches_layer++;
     st->launches_all++;

@@ -61,10 +61,10 @@ def single_codeword_l2(latency_ms):
         return {}
     prof = json.loads(path.read_text())
     return {"l2_bytes_per_decode": prof["l2_bytes"], "l2_gbs": prof["l2_bytes"] / latency_ms / 1e6,
-            "l2_source": path.name, "layer_launches_profiled": prof["launches"],
-            "bound": "dependent layer steps (~3 us each: L2 round trips + grid barrier), L2 throughput "
+            "l2_source": path.name, "launches_profiled": prof["launches"],
+            "bound": "dependent layer steps (~3 us each: launch + L2 round trips), L2 throughput "
                      f"{prof['time_weighted_pct_of_peak'].get('lts__t_sectors.avg.pct_of_peak_sustained_elapsed', 0):.1f}% "
-                     "of peak per launch under ncu (captured on the per-layer launches: same arithmetic, same bytes)"}
+                     "of peak under ncu"}
 
 def peaks():
     try:
@@ -335,9 +335,8 @@ def run_b200(args):
     fer = float((~conv).mean())
 
     # BASELINE configs[1]: one codeword, the latency of one 50-iteration decode through the
-    # default engine choice (one lane: the persistent per-layer kernel, every sweep in one
-    # cooperative launch with a grid barrier between the 30 merged layers; the 19 MB
-    # working set is L2-resident)
+    # default engine choice (one FP32 lane: the per-layer kernels, 1650 dependent launches in
+    # one graph with programmatic dependent launch; the 19 MB working set is L2-resident)
     st1 = _native.State(plan, 1, args.precision)
     st1.set_llr_synthetic(seed=SEED, snr_idx=0, first_frame=rank * B, snr=SNR)
     st1.set_syndrome(None)
@@ -451,9 +450,8 @@ def run_b200(args):
             "mbit_s": n / (float(np.median(b1_ms)) / 1e3) / 1e6, "decodes": len(b1_ms),
             "update_launches_per_decode": int(b1_launches),
             "note": "device time (CUDA events) of qcl_state_decode with the LLRs resident; one-lane layout, "
-                    "layer_persist_kernel: the whole decode in one cooperative launch, a grid barrier "
-                    "between merged layers (1500 per decode); QCL_PERSIST=0 gives the per-layer launches "
-                    "(1650 per decode, programmatic dependent launch)",
+                    "per-layer kernels in one CUDA graph with programmatic dependent launch (the persistent "
+                    "one-launch kernel, QCL_PERSIST=2, measures the same for one FP32 codeword: DESIGN 3.4)",
             **single_codeword_l2(float(np.median(b1_ms))),
         },
     }

@@ -152,10 +152,11 @@ int qcl_state_kernel_stats(qcl_state *st, int64_t *layer_launches, float *layer_
  * decode, tiles ordered by completion flags; FP32, row degree <= 12, >= 4 lanes -- other
  * cases and single-layer calls use engine 0), 0 = TMA-pipelined per-layer kernels,
  * 1 = direct register-staged kernels; 2 / 3 / 6 = engine 0 / 1 / 4 with CUDA events
- * around every sweep or flow launch (read by qcl_state_kernel_stats).  Decodes of one or
- * two codewords on engine 0 / 4 (lane rows narrower than 16 bytes) run every sweep in one
- * cooperative launch of the direct-kernel arithmetic with grid barriers between layers
- * (QCL_PERSIST=0: one launch per layer); engine 1 keeps the per-layer launches. */
+ * around every sweep or flow launch (read by qcl_state_kernel_stats).  FP64 single-codeword
+ * and FP32 two-codeword decodes on engine 0 / 4 (lane rows narrower than 16 bytes) run
+ * every sweep in one cooperative launch of the direct-kernel arithmetic with grid barriers
+ * between layers (QCL_PERSIST=0: one launch per layer, 2: also one FP32 codeword);
+ * engine 1 keeps the per-layer launches. */
 int qcl_state_set_engine(qcl_state *st, int32_t engine);
 
 /* ---- asynchronous path (streaming / overlapped host<->device copies) ---------------

@@ -485,11 +485,15 @@ static void enqueue_sweep(qcl_state *st, double clip, double eps) {
 // bit-identical.  QCL_PERSIST=0 selects the per-layer launches.
 static size_t persist_smem(const qcl_state *st);
 static bool use_persist(const qcl_state *st) {
-    static const int on = env_int("QCL_PERSIST", 1);
-    // engines 0 / 4 where the lane rows are too narrow for bulk copies (engine 1 keeps
-    // the per-layer launches)
-    return on && (st->engine == 0 || st->engine == 4) && st->W <= 2 && !use_tma(st) && !st->msg16 &&
-           persist_smem(st) <= 160 * 1024;
+    // engines 0 / 4 where the lane rows are too narrow for bulk copies (engine 1 keeps the
+    // per-layer launches).  QCL_PERSIST: 1 (default) where it measured faster -- FP64 and
+    // two lanes (one codeword FP64 16.57 -> 14.59 ms, two FP32 5.28 -> 4.89 ms); one FP32
+    // codeword measured 4.44-4.60 ms persistent against 4.42-4.46 per-layer on different
+    // boxes, so it keeps the per-layer graph; 2: every 1-2 lane decode; 0: never.
+    static const int mode = env_int("QCL_PERSIST", 1);
+    const bool fits = (st->engine == 0 || st->engine == 4) && st->W <= 2 && !use_tma(st) && !st->msg16 &&
+                      persist_smem(st) <= 160 * 1024;
+    return fits && (mode == 2 || (mode == 1 && (st->prec == QCL_PREC_FP64 || st->W == 2)));
 }
 
 template <typename T, bool SYN>

@@ -55,10 +55,13 @@ def test_persist_bit_identical_to_layer_launches(gpu, name, batch, precision, en
     ref.decode(cfg)
     want, want_res = ref.download(), ref.results()
     assert ref.kernel_stats()[0] > iters  # engine 1: one launch per launch unit
+    # default QCL_PERSIST=1: the persistent kernel runs FP64 and two-lane decodes (one FP32
+    # codeword keeps the per-layer graph, measured as fast)
+    persistent = precision == "fp64" or batch == 2
     for trial in range(3):  # repeated decodes on one state (barrier words reset per launch)
         per.decode(cfg)
         if not et:
-            assert per.kernel_stats()[0] == 1  # the whole decode in one cooperative launch
+            assert (per.kernel_stats()[0] == 1) == persistent  # the whole decode in one cooperative launch
         got = per.download()
         assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1]), trial
         for a, b in zip(per.results(), want_res):
@@ -76,7 +79,8 @@ def test_persist_concurrent_threads(gpu):
 
     base, sched, index = load_code("standin_v2_z100")
     n, m = base.n_cols * base.z, base.n_rows * base.z
-    dec = q.LayeredDecoder(index, sched, q.DecoderConfig(max_iterations=20, early_termination=False))
+    dec = q.LayeredDecoder(index, sched, q.DecoderConfig(max_iterations=20, early_termination=False),
+                           precision="fp64")
     frames = [channel_llrs(n, 0.2, seed=5, snr_idx=0, frames=1, start=i) for i in range(12)]
     syn = np.zeros((1, m), np.uint8)
     want = [dec.decode_batch_arrays(f, syn) for f in frames]

@@ -1,11 +1,11 @@
 """Persistent per-layer engine (W <= 2 lanes, one cooperative launch per decode) against
-the per-layer launches: run once with QCL_PERSIST=1 and once with QCL_PERSIST=0 (the
+the per-layer launches: run once with QCL_PERSIST=2 (every 1-2 lane decode) and once with QCL_PERSIST=0 (the
 switch is read once per process), then compare.
 
-    QCL_PERSIST=1 python tools/persist_check.py dump gpurun_out/persist_on.npz
+    QCL_PERSIST=2 python tools/persist_check.py dump gpurun_out/persist_on.npz
     QCL_PERSIST=0 python tools/persist_check.py dump gpurun_out/persist_off.npz
     python tools/persist_check.py compare gpurun_out/persist_on.npz gpurun_out/persist_off.npz
-    QCL_PERSIST_BAR=1 python tools/persist_check.py time    # 50-iteration latency, B = 1, 2
+    QCL_PERSIST=2 QCL_PERSIST_BAR=1 python tools/persist_check.py time    # 50-iteration latency, B = 1, 2
 
 `dump` also prints the single-codeword (configs[1]) 50-iteration latency.
 """

@@ -5,6 +5,8 @@
         lts__t_sectors.avg.pct_of_peak_sustained_elapsed,sm__throughput.avg.pct_of_peak_sustained_elapsed \
         python tools/single_codeword_profile.py
     python tools/single_codeword_profile.py --summarize gpurun_out/sc.csv > profiles/r02_single_codeword_l2.json
+    (QCL_PERSIST=0: the per-layer graph, r02_single_codeword_l2.json; default: the persistent
+    kernel, r02_single_codeword_persist_l2.json, read by bench.py)
 
 The first mode decodes one codeword twice and opens the profiler range around the second
 decode only (every launch of one decode).  The second mode sums the per-launch metrics.
@@ -49,7 +51,9 @@ if len(sys.argv) > 2 and sys.argv[1] == "--summarize":
     n_launch = sum(len(v) for v in launches.values())
     t_ns = tot["gpu__time_duration.sum"]
     out = {
-        "workload": "configs[1]: one codeword, standin_v2_z2500, SNR 0.161, 50 iterations, no ET, FP32, per-layer graph",
+        "workload": "configs[1]: one codeword, standin_v2_z2500, SNR 0.161, 50 iterations, no ET, FP32, "
+                    + ("persistent per-layer kernel (one cooperative launch)" if any("layer_persist_kernel" in k for k in per)
+                       else "per-layer graph"),
         "launches": n_launch,
         "serialized_kernel_ms": t_ns / 1e6,
         "l2_bytes": tot["lts__t_bytes.sum"],
@@ -58,8 +62,8 @@ if len(sys.argv) > 2 and sys.argv[1] == "--summarize":
         "mean_launch_us": t_ns / 1e3 / max(n_launch, 1),
         "time_weighted_pct_of_peak": {m: v / t_ns for m, v in pct.items()},
         "per_kernel": {k: {"launches": len(launches[k]), **{m: v for m, v in per[k].items()}} for k in per},
-        "note": "ncu serialises launches and drops the programmatic-dependent-launch overlap; durations "
-                "are cold per launch. L2 bytes and DRAM bytes are per decode.",
+        "note": "ncu serialises launches (and drops the programmatic-dependent-launch overlap of the "
+                "per-layer graph); durations are cold per launch. L2 bytes and DRAM bytes are per decode.",
     }
     print(json.dumps(out, indent=1))
     sys.exit(0)

@@ -252,3 +252,29 @@ def test_fused_et_converging_frames_nonzero_targets(gpu, z):
     assert 5 < c.sum() < B - 5 and len(set(it[c].tolist())) >= 3  # a spread of convergence sweeps
     got_syn = np.stack([w[:, r].sum(axis=1) & 1 for r in rows], axis=1).astype(np.uint8)
     assert np.array_equal(got_syn[c], syn[c])
+
+
+@pytest.mark.parametrize("batch,snr", [(128, 1.5), (21, 1.5), (64, 1.0), (136, 1.0), (40, 1.2)])
+def test_fused_et_all_frames_converge(gpu, batch, snr):
+    """Fused ET where every frame converges well before the cap: the static-order kernel's
+    CTAs stop taking items and every wait that points at a stopped CTA's tile is abandoned
+    (flow.cuh kSpinAborted / consumers_sync_or).  Repeated decodes must terminate and equal
+    the per-layer engine's per-sweep check bit for bit."""
+    from paper_2004_09084_b200 import _native
+    import paper_2004_09084_b200 as q
+
+    base, sched, index = load_code("standin_v2_z100")
+    plan = _native.Plan(index, sched, 0)
+    cfg = _native.make_config(q.DecoderConfig(max_iterations=50, early_termination=True), "fp32")
+    outs = []
+    for engine in (0, 4, 4, 4, 4):
+        st = _native.State(plan, batch, "fp32")
+        st.set_engine(engine)
+        st.set_llr_synthetic(seed=9, snr_idx=2, first_frame=0, snr=snr, encode_mode=True)
+        st.decode(cfg)
+        outs.append(st.results())
+    want = outs[0]
+    assert want[1].all() and want[2].max() < 50, (want[1].mean(), want[2].max())  # every frame converged early
+    for got in outs[1:]:
+        for a, b in zip(got, want):
+            assert np.array_equal(a, b)
